@@ -1,0 +1,137 @@
+"""Oracle nodal-DG right-hand side f(Q, t) for the 3D Euler equations.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Follows, step by step, SURVEY §8(c) O4 -- the nodal strong form of the
+paper's weak formulation ``eq:dgma`` with the semi-discrete ODE
+``eq:ode``:
+
+  1. primitives at every node; rho <= 0, p <= 0 or non-finite -> BlowUp
+  2. Euler fluxes F, G, H (Eq. 1, reading A1)
+  3. volume:   rhs = - sum_d sum_xi  xi_d (D_xi F_d)     (physical-derivative form)
+  4. traces:   q- = Q[vmapM], q+ = Q[vmapP] or a ghost (wall: Eq. 4 / A2;
+               pass-through: Eq. 3 / P:154; inflow: Eqs. 5-7, NEXT N1)
+  5. lambda_f = max over the face's nodes of max(|u-.n| + c-, |u+.n| + c+)
+               (lambda_mode 0) or per node (lambda_mode 1)
+  6. F* = 1/2 n.(F(q-) + F(q+)) - 1/2 lambda (q+ - q-)
+  7. rhs += LIFT (Fscale * (n.F(q-) - F*))
+
+State layout (5, K, Np): field-major, element, node (the public ABI layout).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import conn, euler, geom
+from .refelem import reference_element
+
+BC_INTERIOR, BC_WALL, BC_PASSTHROUGH, BC_INFLOW = 0, 1, 2, 3
+
+
+class BlowUp(RuntimeError):
+    def __init__(self, element: int, t: float, what: str):
+        super().__init__(f"invalid state ({what}) in element {element} at t={t}")
+        self.element = element
+        self.t = t
+
+
+@dataclass
+class OracleMesh:
+    order: int
+    vxyz: np.ndarray
+    etov: np.ndarray
+    bc: np.ndarray
+    gamma: float = 1.4
+    q_inf: tuple = (1.4, 0.0, 0.0, 0.0, 2.5)
+    etoe: np.ndarray | None = None
+    etof: np.ndarray | None = None
+    lambda_mode: int = 0
+    inflow_alpha: float = 565.0
+    _maps: dict = field(default_factory=dict, repr=False)
+
+    def __post_init__(self):
+        self.vxyz = np.asarray(self.vxyz, dtype=np.float64)
+        self.etov = np.asarray(self.etov, dtype=np.int64)
+        self.bc = np.asarray(self.bc, dtype=np.int64)
+        self.ref = reference_element(self.order)
+        self.K = self.etov.shape[0]
+        self.Np = self.ref.Np
+        self.Nfp = self.ref.Nfp
+        self.geo = geom.geometric_factors(self.vxyz, self.etov)
+        if self.etoe is None:
+            self.etoe, self.etof = conn.connect_by_hashing(self.etov)
+        else:
+            self.etoe = np.asarray(self.etoe, dtype=np.int64)
+            self.etof = np.asarray(self.etof, dtype=np.int64)
+            conn.check_symmetric(self.etoe, self.etof)
+        bnd = conn.is_boundary(self.etoe, self.etof)
+        if np.any(bnd & (self.bc == BC_INTERIOR)):
+            raise ValueError("boundary face without a boundary tag")
+        if np.any(~bnd & (self.bc != BC_INTERIOR)):
+            raise ValueError("interior face carries a boundary tag")
+        self.x = geom.node_coordinates(self.vxyz, self.etov, self.ref.r, self.ref.s, self.ref.t)
+
+    def vmaps(self, elems=None):
+        key = None if elems is None else tuple(np.asarray(elems).tolist())
+        if key not in self._maps:
+            self._maps[key] = conn.build_vmaps(self.x, self.vxyz, self.etov, self.etoe, self.etof,
+                                               self.ref.Fmask, self.geo.h, elems)
+        return self._maps[key]
+
+
+def _check_state(mesh: OracleMesh, q: np.ndarray, elems: np.ndarray, t: float):
+    rho, u, v, w, p = euler.primitives(q, mesh.gamma)
+    bad = ~(np.isfinite(q).all(axis=0) & (rho > 0) & (p > 0))
+    if np.any(bad):
+        e = int(elems[np.argwhere(bad.any(axis=-1))[0][0]])
+        raise BlowUp(e, t, "rho<=0, p<=0 or non-finite")
+
+
+def rhs(mesh: OracleMesh, Q: np.ndarray, t: float = 0.0, elems=None) -> np.ndarray:
+    """f(Q, t) for the elements ``elems`` (default: all), shape (5, E, Np)."""
+    ref, g, gamma = mesh.ref, mesh.geo, mesh.gamma
+    K, Np, Nfp = mesh.K, mesh.Np, mesh.Nfp
+    Q = np.asarray(Q, dtype=np.float64)
+    assert Q.shape == (5, K, Np)
+    e = np.arange(K) if elems is None else np.asarray(elems, dtype=np.int64)
+    Qe = Q[:, e]
+    _check_state(mesh, Qe, e, t)
+
+    # steps 2-3: volume term
+    F, G, H = euler.euler_fluxes(Qe, gamma)
+    out = np.zeros_like(Qe)
+    for a, D in enumerate((ref.Dr, ref.Ds, ref.Dt)):
+        for d, Fd in enumerate((F, G, H)):
+            out -= g.rx[e, a, d][None, :, None] * (Fd @ D.T)
+
+    # step 4: traces and ghosts
+    vmapM, vmapP = mesh.vmaps(None if elems is None else e)
+    Qf = Q.reshape(5, K * Np)
+    qm = Qf[:, vmapM]                               # (5, E, 4, Nfp)
+    qp = Qf[:, vmapP].copy()
+    n = np.moveaxis(g.nx[e], 2, 0)[..., None]       # (3, E, 4, 1)
+    tag = mesh.bc[e]                                # (E, 4)
+    wall = tag == BC_WALL
+    if np.any(wall):
+        qp[:, wall] = euler.ghost_wall(qm[:, wall], n[:, wall])
+    pt = tag == BC_PASSTHROUGH
+    if np.any(pt):
+        qp[:, pt] = euler.ghost_passthrough(qm[:, pt], mesh.q_inf)
+    inf = tag == BC_INFLOW
+    if np.any(inf):                                 # NEXT row N1, scaled units of Eq. 3 only
+        p1 = np.full(qm[0, inf].shape, float(euler.inflow_pressure(t, mesh.inflow_alpha)))
+        qp[:, inf] = euler.ghost_inflow(p1, gamma)
+
+    # steps 5-6: LLF flux
+    lam = euler.llf_lambda(qm, qp, n, gamma)        # (E, 4, Nfp)
+    if mesh.lambda_mode == 0:
+        lam = lam.max(axis=2, keepdims=True)
+    fm = euler.normal_flux(qm, n, gamma)
+    fstar = euler.llf_flux(qm, qp, n, gamma, lam)
+
+    # step 7: lift
+    dF = (fm - fstar) * g.Fscale[e][None, :, :, None]
+    out += dF.reshape(5, len(e), 4 * Nfp) @ ref.LIFT.T
+    return out
