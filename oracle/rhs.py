@@ -71,13 +71,29 @@ class OracleMesh:
             raise ValueError("boundary face without a boundary tag")
         if np.any(~bnd & (self.bc != BC_INTERIOR)):
             raise ValueError("interior face carries a boundary tag")
-        self.x = geom.node_coordinates(self.vxyz, self.etov, self.ref.r, self.ref.s, self.ref.t)
+        self._x = None
+
+    @property
+    def x(self):
+        """Node coordinates (3, K, Np), computed on first use (large meshes: use vmaps(elems))."""
+        if self._x is None:
+            self._x = geom.node_coordinates(self.vxyz, self.etov, self.ref.r, self.ref.s, self.ref.t)
+        return self._x
 
     def vmaps(self, elems=None):
         key = None if elems is None else tuple(np.asarray(elems).tolist())
         if key not in self._maps:
-            self._maps[key] = conn.build_vmaps(self.x, self.vxyz, self.etov, self.etoe, self.etof,
-                                               self.ref.Fmask, self.geo.h, elems)
+            if elems is None or self._x is not None:
+                self._maps[key] = conn.build_vmaps(self.x, self.vxyz, self.etov, self.etoe, self.etof,
+                                                   self.ref.Fmask, self.geo.h, elems)
+            else:
+                # sampled use on a large mesh: coordinates of the elements and their neighbours only
+                e = np.asarray(elems, dtype=np.int64)
+                patch = np.unique(np.concatenate([e, self.etoe[e].ravel()]))
+                xs = np.zeros((3, self.K, self.Np))
+                xs[:, patch] = geom.node_coordinates(self.vxyz, self.etov[patch], self.ref.r, self.ref.s, self.ref.t)
+                self._maps[key] = conn.build_vmaps(xs, self.vxyz, self.etov, self.etoe, self.etof,
+                                                   self.ref.Fmask, self.geo.h, e)
         return self._maps[key]
 
 

@@ -1,0 +1,606 @@
+// C-ABI entry points of libdg_b200 (include/dg.h): workspace binding, state
+// I/O, RHS and RK stepping on sm_100a, NCCL face-trace halo exchange.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ctx.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+dg_status set_err(dg_ctx* c, dg_status st, const std::string& m) {
+  if (c) c->err = m;
+  g_err = m;
+  return st;
+}
+
+#define CUDA_TRY(c, x)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err(c, DG_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+
+#define NCCL_TRY(c, x)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess) return set_err(c, DG_ENCCL, std::string("NCCL: ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+// Carpenter & Kennedy (1994) five-stage fourth-order 2N-storage RK (BASELINE.json configs)
+const double LSERK_A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                           -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+const double LSERK_B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                           1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                           2277821191437.0 / 14882151754819.0};
+const double LSERK_C[5] = {0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+                           2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0};
+// Heun = the paper's RK2 in the same 2N-storage form
+const double HEUN_A[2] = {0.0, -1.0};
+const double HEUN_B[2] = {1.0, 0.5};
+const double HEUN_C[2] = {0.0, 1.0};
+
+int nstages(const dg_ctx* c) { return c->rk_scheme == DG_RK_HEUN ? 2 : 5; }
+void coeffs(const dg_ctx* c, int s, double& a, double& b, double& cc) {
+  if (c->rk_scheme == DG_RK_HEUN) {
+    a = HEUN_A[s]; b = HEUN_B[s]; cc = HEUN_C[s];
+  } else {
+    a = LSERK_A[s]; b = LSERK_B[s]; cc = LSERK_C[s];
+  }
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// ---------------------------------------------------------------- kernel dispatch
+template <int N, int MODE>
+cudaError_t launch_stage_n(const dgk::StageArgs& A, cudaStream_t st) {
+  using T = dgk::Tile<N>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgk::stage_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(T::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ntiles = (A.e_end - A.e_begin + T::EB - 1) / T::EB;
+  if (ntiles <= 0) return cudaSuccess;
+  const int grid = std::min(ntiles, num_sms());
+  dgk::stage_kernel<N, MODE><<<grid, T::NT, T::SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_stage(int N, const dgk::StageArgs& A, cudaStream_t st) {
+  switch (N) {
+    case 1: return launch_stage_n<1, MODE>(A, st);
+    case 2: return launch_stage_n<2, MODE>(A, st);
+    case 3: return launch_stage_n<3, MODE>(A, st);
+    case 4: return launch_stage_n<4, MODE>(A, st);
+    case 5: return launch_stage_n<5, MODE>(A, st);
+    case 6: return launch_stage_n<6, MODE>(A, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pack(dg_ctx* c, cudaStream_t st) {
+  if (c->nsend == 0) return cudaSuccess;
+  const int threads = 256;
+  const int64_t total = c->nsend * 5 * c->Nfp;
+  const int grid = int(std::min<int64_t>((total + threads - 1) / threads, 8 * num_sms()));
+  const double* Q = c->dQ[c->cur];
+  switch (c->N) {
+#define PACK(NN) case NN: dgk::pack_kernel<NN><<<grid, threads, 0, st>>>(Q, c->dselem, c->dsface, c->dtbl + 2 * 96 * c->Nfp, c->dsend, c->nsend); break;
+    PACK(1) PACK(2) PACK(3) PACK(4) PACK(5) PACK(6)
+#undef PACK
+  }
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+dgk::StageArgs base_args(dg_ctx* c, double t) {
+  dgk::StageArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.Qin = c->dQ[c->cur];
+  A.Qout = c->dQ[c->cur ^ 1];
+  A.res = c->dres;
+  A.geo = c->dgeo;
+  A.nbr = c->dnbr;
+  A.code = c->dcode;
+  A.pub = c->dpub;
+  A.recv = c->drecv;
+  A.op = c->dop;
+  A.tbl = c->dtbl;
+  A.tblf = c->dtbl + 96 * c->Nfp;
+  A.fmask = c->dtbl + 2 * 96 * c->Nfp;
+  A.flag = c->dflag;
+  A.gid = c->dgid;
+  A.Kpub = int(c->K);
+  A.gamma = c->gamma;
+  A.t = t;
+  for (int i = 0; i < 5; ++i) A.qinf[i] = c->q_inf[i];
+  A.inflow_alpha = c->inflow_alpha;
+  A.lambda_mode = c->lambda_mode;
+  return A;
+}
+
+void set_range(dg_ctx* c, dgk::StageArgs& A, int which) {
+  A.e_begin = (which & 1) ? 0 : int(c->K_int);
+  A.e_end = (which & 2) ? int(c->K) : int(c->K_int);
+}
+
+dg_status need_bound(dg_ctx* c) {
+  if (!c) return set_err(c, DG_EARG, "ctx is NULL");
+  if (!c->ws) return set_err(c, DG_ESTATE, "no workspace bound");
+  return DG_OK;
+}
+
+dg_status halo_exchange(dg_ctx* c, cudaStream_t st) {
+  if (c->nparts == 1 || c->peers.empty()) return DG_OK;
+  if (!c->comm) return set_err(c, DG_ESTATE, "nparts > 1 needs dg_comm_init (or the dg_stage_* driver)");
+  CUDA_TRY(c, launch_pack(c, st));
+  cudaStream_t cs = static_cast<cudaStream_t>(c->comm_stream);
+  CUDA_TRY(c, cudaEventRecord(static_cast<cudaEvent_t>(c->ev_packed), st));
+  CUDA_TRY(c, cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->ev_packed), 0));
+  const size_t rec = size_t(5) * c->Nfp;
+  ncclComm_t comm = static_cast<ncclComm_t>(c->comm);
+  NCCL_TRY(c, ncclGroupStart());
+  for (const dg_peer& p : c->peers) {
+    if (p.nsend) NCCL_TRY(c, ncclSend(c->dsend + p.send_off * rec, p.nsend * rec, ncclDouble, p.rank, comm, cs));
+    if (p.nrecv) NCCL_TRY(c, ncclRecv(c->drecv + p.recv_off * rec, p.nrecv * rec, ncclDouble, p.rank, comm, cs));
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  CUDA_TRY(c, cudaEventRecord(static_cast<cudaEvent_t>(c->ev_recvd), cs));
+  return DG_OK;
+}
+
+dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st) {
+  double a, b, cc;
+  coeffs(c, s, a, b, cc);
+  dgk::StageArgs A = base_args(c, c->t + cc * dt);
+  A.a = a;
+  A.b = b;
+  A.dt = dt;
+  set_range(c, A, which);
+  if (A.e_end > A.e_begin) {
+    CUDA_TRY(c, launch_stage<dgk::MODE_UPDATE>(c->N, A, st));
+    ++c->launches;
+  }
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dg_last_error(const dg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+dg_status dg_mesh_create(const dg_mesh_desc* desc, int rank, dg_ctx** out) {
+  if (!out) return set_err(nullptr, DG_EARG, "out is NULL");
+  *out = nullptr;
+  dg_ctx* c = new dg_ctx();
+  dg_status st = dgb::build_ctx(desc, rank, c);
+  if (st != DG_OK) {
+    g_err = c->err;
+    delete c;
+    return st;
+  }
+  *out = c;
+  return DG_OK;
+}
+
+void dg_destroy(dg_ctx* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(static_cast<ncclComm_t>(c->comm));
+  if (c->comm_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->comm_stream));
+  if (c->ev_packed) cudaEventDestroy(static_cast<cudaEvent_t>(c->ev_packed));
+  if (c->ev_recvd) cudaEventDestroy(static_cast<cudaEvent_t>(c->ev_recvd));
+  delete c;
+}
+
+dg_status dg_sizes(const dg_ctx* c, int64_t* k, int* np, int* nfp) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  if (k) *k = c->K;
+  if (np) *np = c->Np;
+  if (nfp) *nfp = c->Nfp;
+  return DG_OK;
+}
+
+size_t dg_workspace_bytes(const dg_ctx* c) {
+  if (!c) return 0;
+  const size_t st = size_t(c->K) * 5 * c->Np * 8;
+  size_t b = 0;
+  b += 2 * align256(st);                                           // Q ping-pong
+  b += align256(st);                                               // res
+  b += align256(st);                                               // staging
+  b += align256(size_t(c->K) * dgk::GEO * 8);                      // geo
+  b += align256(size_t(c->K) * 16) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 8);
+  b += align256(c->opfrag.size() * 8) + align256(2 * 96 * c->Nfp + 4 * c->Nfp);
+  const size_t rec = size_t(5) * c->Nfp * 8;
+  b += align256(c->nsend * rec) + align256(c->nrecv * rec) + align256(c->nsend * 4) + align256(c->nsend);
+  b += align256(64) + align256(4096 * 8);
+  return b;
+}
+
+dg_status dg_memory_report(const dg_ctx* c, size_t bytes[7]) {
+  if (!c || !bytes) return set_err(nullptr, DG_EARG, "NULL argument");
+  const size_t st = size_t(c->K) * 5 * c->Np * 8;
+  const size_t rec = size_t(5) * c->Nfp * 8;
+  bytes[0] = 2 * st;
+  bytes[1] = st;
+  bytes[2] = st;
+  bytes[3] = size_t(c->K) * dgk::GEO * 8;
+  bytes[4] = size_t(c->K) * (16 + 4 + 4 + 8);
+  bytes[5] = c->opfrag.size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp;
+  bytes[6] = (c->nsend + c->nrecv) * rec + c->nsend * 5;
+  return DG_OK;
+}
+
+dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) {
+  if (!c || !dptr) return set_err(c, DG_EARG, "NULL argument");
+  if (nbytes < dg_workspace_bytes(c)) return set_err(c, DG_EARG, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(dptr) % 256) return set_err(c, DG_EARG, "workspace must be 256-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* p = static_cast<char*>(dptr);
+  auto take = [&](size_t n) {
+    char* r = p;
+    p += align256(n);
+    return r;
+  };
+  const size_t stb = size_t(c->K) * 5 * c->Np * 8;
+  c->dQ[0] = reinterpret_cast<double*>(take(stb));
+  c->dQ[1] = reinterpret_cast<double*>(take(stb));
+  c->dres = reinterpret_cast<double*>(take(stb));
+  c->dstage = reinterpret_cast<double*>(take(stb));
+  c->dgeo = reinterpret_cast<double*>(take(size_t(c->K) * dgk::GEO * 8));
+  c->dnbr = reinterpret_cast<int32_t*>(take(size_t(c->K) * 16));
+  c->dcode = reinterpret_cast<uint8_t*>(take(size_t(c->K) * 4));
+  c->dpub = reinterpret_cast<int32_t*>(take(size_t(c->K) * 4));
+  c->dgid = reinterpret_cast<int64_t*>(take(size_t(c->K) * 8));
+  c->dop = reinterpret_cast<double*>(take(c->opfrag.size() * 8));
+  c->dtbl = reinterpret_cast<uint8_t*>(take(2 * 96 * c->Nfp + 4 * c->Nfp));
+  const size_t rec = size_t(5) * c->Nfp * 8;
+  c->dsend = reinterpret_cast<double*>(take(c->nsend * rec));
+  c->drecv = reinterpret_cast<double*>(take(c->nrecv * rec));
+  c->dselem = reinterpret_cast<int32_t*>(take(c->nsend * 4));
+  c->dsface = reinterpret_cast<uint8_t*>(take(c->nsend));
+  c->dflag = reinterpret_cast<int*>(take(64));
+  c->dscratch = reinterpret_cast<double*>(take(4096 * 8));
+  c->ws = dptr;
+  c->ws_bytes = nbytes;
+  dg_memory_report(c, c->cat_bytes);
+  CUDA_TRY(c, cudaMemcpyAsync(c->dgeo, c->geo.data(), c->geo.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dnbr, c->nbr.data(), c->nbr.size() * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dcode, c->code.data(), c->code.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dpub, c->pub.data(), c->pub.size() * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dgid, c->gid.data(), c->gid.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dop, c->opfrag.data(), c->opfrag.size() * 8, cudaMemcpyHostToDevice, st));
+  std::vector<uint8_t>& tb = c->tbl;  // concatenated tables live until the copy completes (synced below)
+  std::vector<uint8_t> all(tb);
+  all.insert(all.end(), c->tblf.begin(), c->tblf.end());
+  all.insert(all.end(), c->fmask8.begin(), c->fmask8.end());
+  CUDA_TRY(c, cudaMemcpyAsync(c->dtbl, all.data(), all.size(), cudaMemcpyHostToDevice, st));
+  if (c->nsend) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->dselem, c->send_elem.data(), c->nsend * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->dsface, c->send_face.data(), c->nsend, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(c, cudaMemsetAsync(c->dflag, 0, 64, st));
+  CUDA_TRY(c, cudaMemsetAsync(c->dQ[0], 0, 3 * align256(stb), st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));   // host vectors above are pageable / temporaries
+  return DG_OK;
+}
+
+dg_status dg_get_nodes(const dg_ctx* c, double* x, double* y, double* z) {
+  if (!c || !x || !y || !z) return set_err(nullptr, DG_EARG, "NULL argument");
+  const size_t n = size_t(c->K) * c->Np;
+  std::memcpy(x, c->xyz.data(), n * 8);
+  std::memcpy(y, c->xyz.data() + n, n * 8);
+  std::memcpy(z, c->xyz.data() + 2 * n, n * 8);
+  return DG_OK;
+}
+
+dg_status dg_set_state(dg_ctx* c, const double* rho, const double* mx, const double* my, const double* mz,
+                       const double* E, int on_device, double t, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!rho || !mx || !my || !mz || !E) return set_err(c, DG_EARG, "NULL state array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t n = size_t(c->K) * c->Np;
+  const double* src[5] = {rho, mx, my, mz, E};
+  for (int q = 0; q < 5; ++q)
+    CUDA_TRY(c, cudaMemcpyAsync(c->dstage + q * n, src[q], n * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  const int threads = 256;
+  const int grid = int(std::min<int64_t>((int64_t(n) * 5 + threads - 1) / threads, 16 * num_sms()));
+  c->cur = 0;
+  dgk::to_internal_kernel<<<grid, threads, 0, st>>>(c->dstage, c->dpub, c->dQ[0], c->dres, c->K, c->Np);
+  ++c->launches;
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemsetAsync(c->dflag, 0, 64, st));
+  c->t = t;
+  c->state_set = true;
+  c->steps_done = 0;
+  return DG_OK;
+}
+
+dg_status dg_get_state(dg_ctx* c, double* rho, double* mx, double* my, double* mz, double* E, int on_device,
+                       void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!rho || !mx || !my || !mz || !E) return set_err(c, DG_EARG, "NULL state array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t n = size_t(c->K) * c->Np;
+  const int threads = 256;
+  const int grid = int(std::min<int64_t>((int64_t(n) * 5 + threads - 1) / threads, 16 * num_sms()));
+  dgk::to_public_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], c->dpub, c->dstage, c->K, c->Np);
+  ++c->launches;
+  CUDA_TRY(c, cudaGetLastError());
+  double* dst[5] = {rho, mx, my, mz, E};
+  for (int q = 0; q < 5; ++q)
+    CUDA_TRY(c, cudaMemcpyAsync(dst[q], c->dstage + q * n, n * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  return DG_OK;
+}
+
+dg_status dg_get_time(const dg_ctx* c, double* t) {
+  if (!c || !t) return set_err(nullptr, DG_EARG, "NULL argument");
+  *t = c->t;
+  return DG_OK;
+}
+
+dg_status dg_check(dg_ctx* c, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  int h[2] = {0, 0};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->dflag, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  if (h[0]) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "invalid state (rho<=0, p<=0 or non-finite) in element %d at t=%.17g", h[1], c->t);
+    return set_err(c, DG_EBLOWUP, buf);
+  }
+  return DG_OK;
+}
+
+dg_status dg_rhs_compute(dg_ctx* c, double t, double* out, int which, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!out) return set_err(c, DG_EARG, "out is NULL");
+  if (!c->state_set) return set_err(c, DG_ESTATE, "state not set");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dgk::StageArgs A = base_args(c, t);
+  A.out = out;
+  set_range(c, A, which);
+  if (A.e_end > A.e_begin) {
+    CUDA_TRY(c, launch_stage<dgk::MODE_RHS>(c->N, A, st));
+    ++c->launches;
+  }
+  return DG_OK;
+}
+
+dg_status dg_rhs(dg_ctx* c, double t, double* out, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (c->nparts > 1 && !c->peers.empty()) {
+    dg_status e = halo_exchange(c, st);
+    if (e) return e;
+    e = dg_rhs_compute(c, t, out, 1, stream);
+    if (e) return e;
+    CUDA_TRY(c, cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(c->ev_recvd), 0));
+    return dg_rhs_compute(c, t, out, 2, stream);
+  }
+  return dg_rhs_compute(c, t, out, 3, stream);
+}
+
+dg_status dg_stage_pack(dg_ctx* c, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  CUDA_TRY(c, launch_pack(c, static_cast<cudaStream_t>(stream)));
+  return DG_OK;
+}
+
+dg_status dg_stage_compute(dg_ctx* c, int s, double dt, int which, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!c->state_set) return set_err(c, DG_ESTATE, "state not set");
+  if (s < 0 || s >= nstages(c)) return set_err(c, DG_EARG, "stage index out of range");
+  return compute_stage(c, s, dt, which, static_cast<cudaStream_t>(stream));
+}
+
+dg_status dg_stage_finish(dg_ctx* c, int s, double dt) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  c->cur ^= 1;
+  if (s == nstages(c) - 1) {
+    c->t += dt;
+    ++c->steps_done;
+  }
+  return DG_OK;
+}
+
+dg_status dg_rk_step(dg_ctx* c, double dt, int nsteps, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!c->state_set) return set_err(c, DG_ESTATE, "state not set");
+  if (nsteps < 0 || !std::isfinite(dt)) return set_err(c, DG_EARG, "bad dt or nsteps");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool multi = c->nparts > 1 && !c->peers.empty();
+  for (int n = 0; n < nsteps; ++n) {
+    for (int s = 0; s < nstages(c); ++s) {
+      if (multi) {
+        dg_status e = halo_exchange(c, st);
+        if (e) return e;
+        e = compute_stage(c, s, dt, 1, st);
+        if (e) return e;
+        CUDA_TRY(c, cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(c->ev_recvd), 0));
+        e = compute_stage(c, s, dt, 2, st);
+        if (e) return e;
+      } else {
+        dg_status e = compute_stage(c, s, dt, 3, st);
+        if (e) return e;
+      }
+      dg_stage_finish(c, s, dt);
+    }
+    if (c->check_every > 0 && (c->steps_done % c->check_every) == 0) {
+      dg_status e = dg_check(c, stream);
+      if (e) return e;
+    }
+  }
+  return DG_OK;
+}
+
+dg_status dg_stable_dt(dg_ctx* c, double cfl, double* dt, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!dt || !(cfl > 0)) return set_err(c, DG_EARG, "bad argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nn = c->K * c->Np;
+  const int threads = 256;
+  const int grid = int(std::min<int64_t>((nn + threads - 1) / threads, 4096));
+  dgk::max_speed_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], nn, c->Np, c->gamma, c->dscratch);
+  ++c->launches;
+  CUDA_TRY(c, cudaGetLastError());
+  std::vector<double> part(grid);
+  CUDA_TRY(c, cudaMemcpyAsync(part.data(), c->dscratch, grid * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  double lam = 0;
+  for (double v : part) lam = std::max(lam, v);
+  double hmin = *std::min_element(c->h.begin(), c->h.end());
+  if (!(lam > 0) || !std::isfinite(lam)) return set_err(c, DG_EBLOWUP, "non-finite wave speed in stable_dt");
+  *dt = cfl * hmin / ((c->N + 1) * (c->N + 1) * lam);
+  return DG_OK;
+}
+
+dg_status dg_nccl_get_unique_id(void* out128) {
+  if (!out128) return set_err(nullptr, DG_EARG, "NULL argument");
+  ncclUniqueId id;
+  NCCL_TRY(nullptr, ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return DG_OK;
+}
+
+dg_status dg_comm_init(dg_ctx* c, const void* uid, int nranks) {
+  if (!c || !uid) return set_err(c, DG_EARG, "NULL argument");
+  if (nranks != c->nparts) return set_err(c, DG_EARG, "nranks must equal nparts");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm;
+  NCCL_TRY(c, ncclCommInitRank(&comm, nranks, id, c->rank));
+  c->comm = comm;
+  cudaStream_t cs;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  c->comm_stream = cs;
+  cudaEvent_t e1, e2;
+  CUDA_TRY(c, cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+  c->ev_packed = e1;
+  c->ev_recvd = e2;
+  return DG_OK;
+}
+
+dg_status dg_halo_info(const dg_ctx* c, int* npeers, int64_t* nsend, int64_t* nrecv) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  if (npeers) *npeers = int(c->peers.size());
+  if (nsend) *nsend = c->nsend;
+  if (nrecv) *nrecv = c->nrecv;
+  return DG_OK;
+}
+
+dg_status dg_halo_peer(const dg_ctx* c, int p, int* rank, int64_t* send_off, int64_t* nsend, int64_t* recv_off,
+                       int64_t* nrecv) {
+  if (!c || p < 0 || p >= int(c->peers.size())) return set_err(nullptr, DG_EARG, "bad peer index");
+  const dg_peer& q = c->peers[p];
+  if (rank) *rank = q.rank;
+  if (send_off) *send_off = q.send_off;
+  if (nsend) *nsend = q.nsend;
+  if (recv_off) *recv_off = q.recv_off;
+  if (nrecv) *nrecv = q.nrecv;
+  return DG_OK;
+}
+
+dg_status dg_halo_buffers(const dg_ctx* c, double** send, double** recv) {
+  if (!c || !c->ws) return set_err(nullptr, DG_ESTATE, "no workspace bound");
+  if (send) *send = c->dsend;
+  if (recv) *recv = c->drecv;
+  return DG_OK;
+}
+
+dg_status dg_get_operators(const dg_ctx* c, double* r, double* s, double* t, double* Dr, double* Ds, double* Dt,
+                           double* LIFT, int32_t* Fmask) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  const auto& R = c->ref;
+  if (r) std::copy(R.r.begin(), R.r.end(), r);
+  if (s) std::copy(R.s.begin(), R.s.end(), s);
+  if (t) std::copy(R.t.begin(), R.t.end(), t);
+  if (Dr) std::copy(R.Dr.begin(), R.Dr.end(), Dr);
+  if (Ds) std::copy(R.Ds.begin(), R.Ds.end(), Ds);
+  if (Dt) std::copy(R.Dt.begin(), R.Dt.end(), Dt);
+  if (LIFT) std::copy(R.LIFT.begin(), R.LIFT.end(), LIFT);
+  if (Fmask)
+    for (size_t i = 0; i < R.Fmask.size(); ++i) Fmask[i] = R.Fmask[i];
+  return DG_OK;
+}
+
+dg_status dg_get_maps(const dg_ctx* c, int64_t* vmapM, int64_t* vmapP) {
+  if (!c || !vmapM || !vmapP) return set_err(nullptr, DG_EARG, "NULL argument");
+  const int Np = c->Np, Nfp = c->Nfp;
+  // reported in PUBLIC element order
+  for (int64_t l = 0; l < c->K; ++l) {
+    const int64_t p = c->pub[l];
+    for (int f = 0; f < 4; ++f) {
+      const int code = c->code[l * 4 + f];
+      for (int i = 0; i < Nfp; ++i) {
+        const int64_t m = p * Np + c->ref.Fmask[f * Nfp + i];
+        const size_t o = (size_t(p) * 4 + f) * Nfp + i;
+        vmapM[o] = m;
+        if (code >= dgk::CODE_BC) {
+          vmapP[o] = m;
+        } else if (code >= dgk::CODE_GHOST) {
+          const int j = c->tblf[(f * 24 + code - dgk::CODE_GHOST) * Nfp + i];
+          vmapP[o] = -1 - (int64_t(c->nbr[l * 4 + f]) * Nfp + j);
+        } else {
+          vmapP[o] = int64_t(c->pub[c->nbr[l * 4 + f]]) * Np + c->tbl[(f * 24 + code) * Nfp + i];
+        }
+      }
+    }
+  }
+  return DG_OK;
+}
+
+dg_status dg_get_geometry(const dg_ctx* c, double* J, double* rx9, double* n12, double* fs4) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  for (int64_t l = 0; l < c->K; ++l) {
+    const int64_t p = c->pub[l];
+    const double* G = &c->geo[l * dgk::GEO];
+    if (J) J[p] = c->J[l];
+    for (int i = 0; i < 9; ++i)
+      if (rx9) rx9[p * 9 + i] = G[i];
+    for (int f = 0; f < 4; ++f) {
+      for (int q = 0; q < 3; ++q)
+        if (n12) n12[p * 12 + 3 * f + q] = G[9 + 4 * f + q];
+      if (fs4) fs4[p * 4 + f] = G[9 + 4 * f + 3];
+    }
+  }
+  return DG_OK;
+}
+
+int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

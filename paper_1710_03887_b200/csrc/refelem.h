@@ -1,0 +1,37 @@
+// Reference tetrahedron for the nodal DG operators (library side, fp64).
+// PAPER.md P:407-414 (Appendix A): orthonormal polynomial basis on each element
+// (mass matrix = multiple of I).  The library builds the nodal operators from
+// that basis -- the orthonormal Dubiner/PKDO polynomials on the reference tet,
+// evaluated with normalised Jacobi recurrences -- entirely in fp64, a route
+// independent of the oracle's (shifted monomials + 50-digit mpmath).
+#pragma once
+#include <string>
+#include <vector>
+
+namespace dgb {
+
+struct RefElem {
+  int N = 0, Np = 0, Nfp = 0;
+  std::vector<double> r, s, t;          // Np node coordinates (ABI order)
+  std::vector<double> Dr, Ds, Dt;       // Np x Np row-major
+  std::vector<double> LIFT;             // Np x 4Nfp row-major, columns face-major
+  std::vector<int> Fmask;               // 4 x Nfp ascending node ids per face
+  // face-local lattice coordinates of each face node: for face f node i, the
+  // integer weights (over N) of the face's three vertices FACE_VERTS[f]
+  std::vector<int> face_lat;            // 4 x Nfp x 3
+  // nbr_local[((f*4 + f2)*6 + sigma)*Nfp + i]: face-local index j on neighbour
+  // face f2 of my face node i when my face vertex m matches neighbour face
+  // vertex PERM[sigma][m]
+  std::vector<int> nbr_local;
+};
+
+extern const int FACE_VERTS[4][3];
+extern const int PERM6[6][3];
+
+inline int n_nodes(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
+inline int n_face_nodes(int N) { return (N + 1) * (N + 2) / 2; }
+
+// Builds everything above; returns false (with msg) on numerical failure.
+bool build_reference(int N, RefElem& R, std::string* msg);
+
+}  // namespace dgb

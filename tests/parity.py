@@ -1,0 +1,46 @@
+"""Parity metrics and shared helpers for the GPU-vs-oracle tests.
+
+Tolerances (BASELINE.json north_star; reading A14): fields are made
+dimensionless by the physical scales S = (rho0, rho0 c0, rho0 c0, rho0 c0, E0)
+because a field can be identically ~0 (e.g. rhs_rho at t = 0 of a pulse at rest):
+
+  e_rhs   = max_q |d rhs_q|_inf / S_q  /  max_q |rhs_q|_inf / S_q   <= 1e-11 (one RHS)
+  e_state = max_q |d Q_q|_inf / S_q                                 <= 1e-9  (100 RK steps)
+"""
+import math
+
+import numpy as np
+
+from oracle import euler
+from oracle.rhs import OracleMesh
+
+RHS_TOL = 1e-11
+STATE_TOL = 1e-9
+
+
+def scales(cfg):
+    c0 = math.sqrt(cfg.gamma * cfg.p0 / cfg.rho0)
+    return np.array([cfg.rho0, cfg.rho0 * c0, cfg.rho0 * c0, cfg.rho0 * c0, cfg.p0 / (cfg.gamma - 1.0)])
+
+
+def e_rhs(gpu, ora, S):
+    d = (np.abs(gpu - ora).reshape(5, -1).max(axis=1) / S).max()
+    m = (np.abs(ora).reshape(5, -1).max(axis=1) / S).max()
+    return d / m
+
+
+def e_state(gpu, ora, S):
+    return (np.abs(gpu - ora).reshape(5, -1).max(axis=1) / S).max()
+
+
+def oracle_mesh(cfg, lambda_mode=0):
+    m = cfg.mesh
+    return OracleMesh(order=cfg.order, vxyz=m.vxyz, etov=m.etov, bc=m.bc, etoe=m.etoe, etof=m.etof,
+                      gamma=cfg.gamma, q_inf=cfg.q_inf, lambda_mode=lambda_mode)
+
+
+def oracle_dt(o: OracleMesh, Q, cfl):
+    """CFL rule of DESIGN.md A10 evaluated by the oracle: cfl h_min / ((N+1)^2 max(|u| + c))."""
+    rho, u, v, w, p = euler.primitives(Q, o.gamma)
+    lam = (np.sqrt(u * u + v * v + w * w) + np.sqrt(o.gamma * p / rho)).max()
+    return cfl * o.geo.h.min() / ((o.order + 1) ** 2 * lam)

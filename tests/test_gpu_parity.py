@@ -1,0 +1,235 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle.
+
+Same seeded inputs on both sides (synth/ recipes at the ORACLE's node
+coordinates); tolerances from BASELINE.json (tests/parity.py):
+  one RHS <= 1e-11 (scaled), 100 LSERK4 steps <= 1e-9.
+Sizes: oracle-sized versions of C1-C5 that span several tiles and a ragged
+tail; full-size C2-C5 in the bench launch configuration on sampled elements;
+edge cases (one element, ragged tails, every boundary kind, lambda modes,
+Heun, inflow), blow-up detection, state round trip, and partition invariance
+(emulated ranks on one GPU, exchange by device copies).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1710_03887_b200 as dg  # noqa: E402
+from oracle import timestep  # noqa: E402
+from oracle.rhs import rhs as oracle_rhs  # noqa: E402
+from synth import configs  # noqa: E402
+from synth import mesh as smesh  # noqa: E402
+
+import parity  # noqa: E402
+
+SMALL = [("C1", 1.0), ("C2", 0.25), ("C3", 0.15), ("C4", 0.1), ("C5", 0.1)]
+
+
+def solver(cfg, **kw):
+    m = cfg.mesh
+    return dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma,
+                     q_inf=cfg.q_inf, **kw)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+@pytest.mark.parametrize("name,scale", SMALL)
+@pytest.mark.parametrize("lambda_mode", [0, 1])
+def test_rhs_parity_small(name, scale, lambda_mode):
+    cfg = configs.make(name, scale=scale)
+    o = parity.oracle_mesh(cfg, lambda_mode)
+    Q = configs.initial_state(cfg, o.x)
+    s = solver(cfg, lambda_mode=lambda_mode)
+    s.set_state(Q)
+    g = s.rhs(0.0)
+    r = oracle_rhs(o, Q)
+    err = parity.e_rhs(g, r, parity.scales(cfg))
+    assert err <= parity.RHS_TOL, err
+    assert dg.dg_launch_count(s.ctx) >= 2
+
+
+@pytest.mark.parametrize("name,scale", SMALL)
+def test_rk_parity_100_steps(name, scale):
+    cfg = configs.make(name, scale=scale)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    dt = parity.oracle_dt(o, Q, cfg.cfl)
+    s = solver(cfg)
+    s.set_state(Q)
+    s.step(dt, 100)
+    g = s.get_state()
+    Qo, _, t = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 100)
+    err = parity.e_state(g, Qo, parity.scales(cfg))
+    assert err <= parity.STATE_TOL, err
+    assert abs(s.time - t) < 1e-12 * max(1.0, t)
+
+
+def test_heun_parity():
+    cfg = configs.make("C3", scale=0.15)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    dt = parity.oracle_dt(o, Q, 0.3)
+    s = solver(cfg, rk_scheme=dg.DG_RK_HEUN)
+    s.set_state(Q)
+    s.step(dt, 20)
+    Qo, _, _ = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 20, scheme="heun")
+    assert parity.e_state(s.get_state(), Qo, parity.scales(cfg)) <= parity.STATE_TOL
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6])
+def test_every_order_and_boundary_kind(N):
+    """Walls, pass-through and an inflow face (NEXT N1) on one distorted box, every order."""
+    m = smesh.kuhn_box((3, 2, 2), (0, 0, 0), (1, 0.7, 0.7), bc_tag=smesh.BC_WALL)
+    rng = np.random.default_rng(N)
+    lo, hi = m.vxyz.min(0), m.vxyz.max(0)
+    inner = np.all((m.vxyz > lo + 1e-9) & (m.vxyz < hi - 1e-9), axis=1)
+    m.vxyz[inner] += rng.uniform(-0.03, 0.03, (int(inner.sum()), 3))
+    cen = m.vxyz[m.etov].mean(axis=1)
+    bnd = m.bc != 0
+    m.bc[bnd & (cen[:, 0:1] > 0.6)] = smesh.BC_PASSTHROUGH
+    m.bc[bnd & (cen[:, 0:1] < 0.2)] = smesh.BC_INFLOW
+    cfg = configs.Config("box", N, m, rho0=1.4, p0=1.0, gamma=1.4,
+                         pulses=[(0.05, 0.2, (0.5, 0.35, 0.35))], steps=1)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    Q[1] += 0.05 * Q[0] * np.sin(3 * o.x[1])          # some flow so every ghost matters
+    Q[4] += 0.5 * (Q[1] ** 2) / Q[0]
+    s = solver(cfg)
+    s.set_state(Q)
+    t = 0.002                                           # inside the inflow pulse
+    err = parity.e_rhs(s.rhs(t), oracle_rhs(o, Q, t), parity.scales(cfg))
+    assert err <= parity.RHS_TOL, err
+
+
+@pytest.mark.parametrize("K", [1, 7, 33, 65])
+def test_ragged_tails(K):
+    cfg = configs.make("C2", scale=0.25)
+    m = cfg.mesh
+    sub = smesh.TetMesh(vxyz=m.vxyz, etov=m.etov[:K], etoe=None, etof=None, bc=None)
+    from oracle.conn import connect_by_hashing
+    e, f = connect_by_hashing(sub.etov)
+    b = (e == np.arange(K)[:, None]) & (f == np.arange(4)[None, :])
+    sub.etoe, sub.etof = e, f
+    sub.bc = np.where(b, smesh.BC_WALL, 0).astype(np.int8)
+    for N in (3, 4):
+        c = configs.Config("sub", N, sub, rho0=1.4, p0=1.0, gamma=1.4, pulses=cfg.pulses, steps=1)
+        o = parity.oracle_mesh(c)
+        Q = configs.initial_state(c, o.x)
+        Q[1] += 0.05 * Q[0] * np.sin(5 * o.x[1] + 1)      # flow, so the rhs is not round-off
+        Q[3] += 0.03 * Q[0] * np.cos(4 * o.x[0])
+        Q[4] += 0.5 * (Q[1] ** 2 + Q[3] ** 2) / Q[0]
+        s = solver(c)
+        s.set_state(Q)
+        assert parity.e_rhs(s.rhs(0.0), oracle_rhs(o, Q), parity.scales(c)) <= parity.RHS_TOL
+
+
+def test_free_stream_and_state_roundtrip():
+    cfg = configs.make("C5", scale=0.1)
+    s = solver(cfg)
+    K, Np = s.K, s.Np
+    Q = np.empty((5, K, Np))
+    for q, v in enumerate((1.3, 0.2, -0.1, 0.3, 3.0)):
+        Q[q] = v
+    s.set_state(Q)
+    assert np.array_equal(s.get_state(), Q)              # bitwise round trip
+    f = s.rhs(0.0)
+    h = dg.dg_get_geometry(s.ctx)["J"]
+    assert np.abs(f).max() < 1e-10 and h.min() > 0
+
+
+def test_blowup_flag_names_the_element():
+    cfg = configs.make("C2", scale=0.25)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    Q[4, 37, 5] = -1.0
+    s = solver(cfg)
+    s.set_state(Q)
+    s.step(1e-4, 1)
+    with pytest.raises(dg.DGError) as e:
+        dg.dg_check(s.ctx, s.stream)
+    assert e.value.status == dg.DG_EBLOWUP and "element 37" in str(e.value)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_sampled(name):
+    """Full BASELINE.json size, bench launch configuration; oracle on sampled elements:
+    one RHS, and stage 0 of the LSERK update (res = dt f, Q += b_0 res)."""
+    cfg = configs.make(name)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    s = solver(cfg)
+    s.set_state(Q)
+    K = cfg.mesh.K
+    rng = np.random.default_rng(0)
+    wall = np.nonzero((cfg.mesh.bc == smesh.BC_WALL).any(axis=1))[0]
+    pt = np.nonzero((cfg.mesh.bc == smesh.BC_PASSTHROUGH).any(axis=1))[0]
+    sample = np.unique(np.concatenate([rng.choice(K, 160, replace=False), wall[:24], pt[:24],
+                                       np.arange(K - 9, K), np.arange(0, 5)]))
+    g = s.rhs(0.0, device=True)[:, torch.as_tensor(sample, device=s.device)].cpu().numpy()
+    r = oracle_rhs(o, Q, 0.0, elems=sample)
+    S = parity.scales(cfg)
+    assert parity.e_rhs(g, r, S) <= parity.RHS_TOL
+    dt = 1e-3
+    dg.dg_stage_compute(s.ctx, 0, dt, 3, s.stream)
+    dg.dg_stage_finish(s.ctx, 0, dt)
+    Q1 = s.get_state(device=True)[:, torch.as_tensor(sample, device=s.device)].cpu().numpy()
+    want = Q[:, sample] + timestep.LSERK4_B[0] * (dt * r)
+    assert parity.e_state(Q1, want, S) <= 1e-14
+
+
+def ws_view(sv, ptr, nbytes):
+    off = ptr - sv.ws.data_ptr()
+    assert 0 <= off and off + nbytes <= sv.ws.numel()
+    return sv.ws[off:off + nbytes]
+
+
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_partition_invariance_emulated(nparts):
+    """P ranks emulated as P contexts on one GPU, halo records exchanged by device
+    copies between the stage-level calls: final state bitwise equal to P = 1."""
+    cfg = configs.make("C4", scale=0.12)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    dt = parity.oracle_dt(o, Q, 0.5)
+    ref = solver(cfg)
+    ref.set_state(Q)
+    ref.step(dt, 10)
+    want = ref.get_state()
+    part = smesh.x_slab_partition(cfg.mesh, nparts)
+    ranks = [solver(cfg, part=part, nparts=nparts, rank=r) for r in range(nparts)]
+    for r, sv in enumerate(ranks):
+        sv.set_state(Q[:, part == r])
+    rec = 5 * ranks[0].Nfp
+    for _ in range(10):
+        for st in range(5):
+            for sv in ranks:
+                dg.dg_stage_pack(sv.ctx, sv.stream)
+            for r, sv in enumerate(ranks):
+                npeer, _, _ = dg.dg_halo_info(sv.ctx)
+                _, rbuf = dg.dg_halo_buffers(sv.ctx)
+                for p in range(npeer):
+                    info = dg.dg_halo_peer(sv.ctx, p)
+                    other = ranks[info["rank"]]
+                    sbuf, _ = dg.dg_halo_buffers(other.ctx)
+                    back = [dg.dg_halo_peer(other.ctx, q) for q in range(dg.dg_halo_info(other.ctx)[0])]
+                    mine = [b for b in back if b["rank"] == r][0]
+                    assert mine["nsend"] == info["nrecv"]
+                    n = info["nrecv"] * rec * 8
+                    if n:   # device-to-device copy through torch views of the two workspaces
+                        dst = ws_view(sv, rbuf + info["recv_off"] * rec * 8, n)
+                        src = ws_view(other, sbuf + mine["send_off"] * rec * 8, n)
+                        dst.copy_(src)
+            for sv in ranks:
+                dg.dg_stage_compute(sv.ctx, st, dt, 3, sv.stream)
+            for sv in ranks:
+                dg.dg_stage_finish(sv.ctx, st, dt)
+    got = np.empty_like(want)
+    for r, sv in enumerate(ranks):
+        got[:, part == r] = sv.get_state()
+    assert np.array_equal(got, want)
