@@ -35,19 +35,26 @@ def pressure(q: np.ndarray, gamma: float = 1.4) -> np.ndarray:
     return primitives(np.asarray(q, dtype=np.float64), gamma)[4]
 
 
-def euler_fluxes(q: np.ndarray, gamma: float):
-    """(F, G, H), each shaped like q: the x, y, z flux vectors of Eq. 1 (reading A1)."""
+def euler_fluxes(q: np.ndarray, gamma: float, p_shift: float = 0.0):
+    """(F, G, H), each shaped like q: the x, y, z flux vectors of Eq. 1 (reading A1).
+
+    ``p_shift`` subtracts the constant flux (0, p_shift e_d, 0) from the momentum rows
+    (reading A14, "background-flux subtraction"): exact for the DG operator,
+    which differentiates constants to zero and whose LLF difference n.F(q-) - F* is
+    invariant under a constant flux shift; it only removes the O(p0) round-off of the
+    ambient pressure."""
     rho, u, v, w, p = primitives(q, gamma)
     E = q[4]
-    F = np.stack([rho * u, rho * u * u + p, rho * u * v, rho * u * w, u * (E + p)])
-    G = np.stack([rho * v, rho * u * v, rho * v * v + p, rho * v * w, v * (E + p)])
-    H = np.stack([rho * w, rho * u * w, rho * v * w, rho * w * w + p, w * (E + p)])
+    pm = p - p_shift
+    F = np.stack([rho * u, rho * u * u + pm, rho * u * v, rho * u * w, u * (E + p)])
+    G = np.stack([rho * v, rho * u * v, rho * v * v + pm, rho * v * w, v * (E + p)])
+    H = np.stack([rho * w, rho * u * w, rho * v * w, rho * w * w + pm, w * (E + p)])
     return F, G, H
 
 
-def normal_flux(q: np.ndarray, n: np.ndarray, gamma: float) -> np.ndarray:
+def normal_flux(q: np.ndarray, n: np.ndarray, gamma: float, p_shift: float = 0.0) -> np.ndarray:
     """n . F(q) with n = (nx, ny, nz) broadcast against q[0]."""
-    F, G, H = euler_fluxes(q, gamma)
+    F, G, H = euler_fluxes(q, gamma, p_shift)
     return n[0] * F + n[1] * G + n[2] * H
 
 
@@ -95,8 +102,9 @@ def llf_lambda(qm: np.ndarray, qp: np.ndarray, n: np.ndarray, gamma: float) -> n
     return np.maximum(speed(qm), speed(qp))
 
 
-def llf_flux(qm: np.ndarray, qp: np.ndarray, n: np.ndarray, gamma: float, lam=None) -> np.ndarray:
+def llf_flux(qm: np.ndarray, qp: np.ndarray, n: np.ndarray, gamma: float, lam=None,
+             p_shift: float = 0.0) -> np.ndarray:
     """F* = 1/2 n.(F(q-) + F(q+)) - 1/2 lam (q+ - q-); lam defaults to the per-node value."""
     if lam is None:
         lam = llf_lambda(qm, qp, n, gamma)
-    return 0.5 * (normal_flux(qm, n, gamma) + normal_flux(qp, n, gamma)) - 0.5 * lam * (qp - qm)
+    return 0.5 * (normal_flux(qm, n, gamma, p_shift) + normal_flux(qp, n, gamma, p_shift)) - 0.5 * lam * (qp - qm)

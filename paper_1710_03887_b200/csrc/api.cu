@@ -138,6 +138,8 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   for (int i = 0; i < 5; ++i) A.qinf[i] = c->q_inf[i];
   A.inflow_alpha = c->inflow_alpha;
   A.lambda_mode = c->lambda_mode;
+  const double* qi = c->q_inf;
+  A.pref = (c->gamma - 1.0) * (qi[4] - 0.5 * (qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]) / qi[0]);
   return A;
 }
 

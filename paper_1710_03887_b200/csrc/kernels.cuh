@@ -48,6 +48,7 @@ struct StageArgs {
   int e_begin, e_end;     // element range of this launch
   int Kpub;
   double gamma, a, b, dt, t;
+  double pref;            // ambient pressure subtracted from the momentum fluxes (exact, A14)
   double qinf[5];
   double inflow_alpha;
   int lambda_mode;
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
       if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(A.flag, A.gid[e0 + e]);
       const double* G = sG + e * GEO;
       const double Ep = E + p;
+      const double pd = p - A.pref;   // background-flux subtraction (A14)
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
@@ -185,9 +187,9 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
         const double U = cx * u + cy * v + cz * w;
         double* xc = xr + d * NP + n;
         xc[0] = rho * U;
-        xc[XS] = mx * U + cx * p;
-        xc[2 * XS] = my * U + cy * p;
-        xc[3 * XS] = mz * U + cz * p;
+        xc[XS] = mx * U + cx * pd;
+        xc[2 * XS] = my * U + cy * pd;
+        xc[3 * XS] = mz * U + cz * pd;
         xc[4 * XS] = Ep * U;
       }
     }
@@ -282,20 +284,22 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
         const double ri = 1.0 / qm[r][0];
         const double un = (qm[r][1] * nx + qm[r][2] * ny + qm[r][3] * nz) * ri;
         const double p = gm1 * (qm[r][4] - 0.5 * (qm[r][1] * qm[r][1] + qm[r][2] * qm[r][2] + qm[r][3] * qm[r][3]) * ri);
+        const double pd = p - A.pref;
         fm[0] = qm[r][0] * un;
-        fm[1] = qm[r][1] * un + p * nx;
-        fm[2] = qm[r][2] * un + p * ny;
-        fm[3] = qm[r][3] * un + p * nz;
+        fm[1] = qm[r][1] * un + pd * nx;
+        fm[2] = qm[r][2] * un + pd * ny;
+        fm[3] = qm[r][3] * un + pd * nz;
         fm[4] = (qm[r][4] + p) * un;
       }
       {
         const double ri = 1.0 / qp[r][0];
         const double un = (qp[r][1] * nx + qp[r][2] * ny + qp[r][3] * nz) * ri;
         const double p = gm1 * (qp[r][4] - 0.5 * (qp[r][1] * qp[r][1] + qp[r][2] * qp[r][2] + qp[r][3] * qp[r][3]) * ri);
+        const double pd = p - A.pref;
         fp[0] = qp[r][0] * un;
-        fp[1] = qp[r][1] * un + p * nx;
-        fp[2] = qp[r][2] * un + p * ny;
-        fp[3] = qp[r][3] * un + p * nz;
+        fp[1] = qp[r][1] * un + pd * nx;
+        fp[2] = qp[r][2] * un + pd * ny;
+        fp[3] = qp[r][3] * un + pd * nz;
         fp[4] = (qp[r][4] + p) * un;
       }
       // dF = Fscale (n.F(q-) - F*),  F* = 1/2 (fm + fp) - 1/2 lam (q+ - q-)
