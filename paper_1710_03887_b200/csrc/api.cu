@@ -87,13 +87,29 @@ cudaError_t launch_stage_n(const dgk::StageArgs& A, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int N, int MODE>
+cudaError_t launch_ws_n(const dgk::StageArgs& A, cudaStream_t st) {
+  using W = dgk::WS<N>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgk::stage_ws_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ntiles = (A.e_end - A.e_begin + W::EB - 1) / W::EB;
+  if (ntiles <= 0) return cudaSuccess;
+  const int grid = std::min(ntiles, num_sms());
+  dgk::stage_ws_kernel<N, MODE><<<grid, W::NT, W::SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
 template <int MODE>
 cudaError_t launch_stage(int N, const dgk::StageArgs& A, cudaStream_t st) {
   switch (N) {
-    case 1: return launch_stage_n<1, MODE>(A, st);
-    case 2: return launch_stage_n<2, MODE>(A, st);
-    case 3: return launch_stage_n<3, MODE>(A, st);
-    case 4: return launch_stage_n<4, MODE>(A, st);
+    case 1: return launch_ws_n<1, MODE>(A, st);
+    case 2: return launch_ws_n<2, MODE>(A, st);
+    case 3: return launch_ws_n<3, MODE>(A, st);
+    case 4: return launch_ws_n<4, MODE>(A, st);
     case 5: return launch_stage_n<5, MODE>(A, st);
     case 6: return launch_stage_n<6, MODE>(A, st);
   }

@@ -2,8 +2,7 @@
 //
 // One fused, persistent kernel per Runge-Kutta stage.  A CTA owns a tile of EB
 // elements at a time:
-//   A. TMA-free coalesced load of the tile's state Q[e][5][Np] and geometric
-//      factors into shared memory;
+//   A. load the tile's state Q[e][5][Np] and geometric factors into shared memory;
 //   B. pointwise volume flux (Eq. 1-2): contravariant fluxes
 //      Ft_xi = xi_x F + xi_y G + xi_z H (xi = r,s,t) written row-major into the
 //      shared operand X[(e,field)][k], k in [0, 3Np);
@@ -11,14 +10,19 @@
 //      the neighbour's Q (vmapP encoded as neighbour element + face-permutation
 //      code) or the halo buffer or a boundary ghost (wall: Eq. 4 mirror,
 //      pass-through: Eq. 3, inflow: Eqs. 5-7), per-node wave speed, face max,
-//      LLF flux, dF = Fscale (n.F(q-) - F*) written to X, k in [3Np, 3Np+4Nfp);
+//      LLF flux, dF = Fscale (n.F(q-) - F*) written to X, k in [KVP, KVP+4Nfp);
 //   D. one dense contraction per tile on the FP64 tensor cores (DMMA,
 //      mma.sync m16n8k4 f64):  rhs[(e,field)][n] = sum_k X[(e,field)][k] Op[n][k]
-//      with Op = [-Dr -Ds -Dt LIFT] (Np x (3Np+4Nfp)) shared by every element,
-//      held in shared memory in B-fragment order;
+//      with Op = [-Dr -Ds -Dt 0 LIFT] (Np x KPAD) shared by every element, held
+//      in shared memory in B-fragment order;
 //   E. epilogue straight from the accumulator fragments: LSERK update
 //      res = a res + dt rhs, Q_out = Q_in + b res (ping-pong Q, so neighbours of
 //      later tiles still read the stage-input state), or rhs written out.
+//
+// stage_ws_kernel (N <= 4) is warp-specialised: 8 producer warps run A-C for
+// tile i+1 while 8 consumer warps run D-E for tile i, handing over the volume
+// and face halves of X through named barriers (bar.arrive / bar.sync).
+// stage_kernel (N = 5, 6) runs A-E in lock-step with __syncthreads.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -59,35 +63,15 @@ struct Shape {
   static constexpr int NP = (N + 1) * (N + 2) * (N + 3) / 6;
   static constexpr int NFP = (N + 1) * (N + 2) / 2;
   static constexpr int KV = 3 * NP;
-  static constexpr int KT = KV + 4 * NFP;
-  static constexpr int KPAD = (KT + 3) / 4 * 4;
+  static constexpr int KVP = (KV + 3) / 4 * 4;        // volume block padded to the DMMA k=4
+  static constexpr int KPAD = KVP + 4 * NFP;          // face block starts at KVP
   static constexpr int KS4 = KPAD / 4;
+  static constexpr int KSV = KVP / 4;                 // k-steps of the volume block
   static constexpr int NPAD = (NP + 7) / 8 * 8;
   static constexpr int NTL = NPAD / 8;
-  // row stride of X in doubles: >= KPAD and == 4 (mod 16) -> conflict-free A fragments
-  static constexpr int XS = ((KPAD + 11) / 16) * 16 + 4;
+  // row stride of X in doubles: >= KPAD and == 12 (mod 16) -> conflict-free A fragments
+  static constexpr int XS = (KPAD + 3) / 16 * 16 + 12;
   static constexpr int OPN = KS4 * NTL * 32;   // doubles in the B-fragment operator
-};
-
-template <int N>
-struct Tile {
-  // elements per tile; rows (element, field) padded to a multiple of 16 (the DMMA M)
-  static constexpr int EB = (N <= 3) ? 32 : (N == 4 ? 16 : 8);
-  static constexpr int NT = 512;
-  static constexpr int ROWS = (5 * EB + 15) / 16 * 16;
-  static constexpr int MT = ROWS / 16;
-  static constexpr bool OP_SMEM = Shape<N>::OPN * 8 <= 72 * 1024;
-  static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;          // n-tiles per work item
-  static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
-  static constexpr int ITEMS = MT * NGRP;
-  static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
-  static constexpr size_t SMEM_OP = OP_SMEM ? size_t(Shape<N>::OPN) * 8 : 0;
-  static constexpr size_t SMEM_Q = size_t(EB) * 5 * Shape<N>::NP * 8;
-  static constexpr size_t SMEM_G = size_t(EB) * GEO * 8;
-  static constexpr size_t SMEM_L = size_t(EB) * 4 * Shape<N>::NFP * 8;
-  static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_Q + SMEM_G + SMEM_L + SMEM_T;
-  static_assert(SMEM <= 227 * 1024, "tile does not fit in shared memory");
 };
 
 __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
@@ -96,6 +80,9 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
       : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
       : "d"(a0), "d"(a1), "d"(b0));
 }
+
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ void flag_blowup(int* flag, int64_t gid) {
   if (atomicCAS(flag, 0, 1) == 0) flag[1] = (int)gid;
@@ -115,6 +102,104 @@ __device__ __forceinline__ void inflow_state(double t, double alpha, double gamm
 
 enum { MODE_UPDATE = 0, MODE_RHS = 1 };
 
+// ---------------------------------------------------------------- pointwise pieces
+// Volume flux at one node: q -> 15 contravariant flux values in X rows e*5+c, cols d*NP+n.
+template <int NP, int XS>
+__device__ __forceinline__ void volume_node(const double* q, const double* G, double* xr, double gm1, double pref,
+                                            int* flag, int64_t gid) {
+  const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
+  const double ri = 1.0 / rho;
+  const double u = mx * ri, v = my * ri, w = mz * ri;
+  const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
+  if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(flag, gid);
+  const double Ep = E + p;
+  const double pd = p - pref;   // background-flux subtraction (A14)
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
+    const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
+    double* xc = xr + d * NP;
+    xc[0] = rho * U;
+    xc[XS] = fma(cx, pd, mx * U);
+    xc[2 * XS] = fma(cy, pd, my * U);
+    xc[3 * XS] = fma(cz, pd, mz * U);
+    xc[4 * XS] = Ep * U;
+  }
+}
+
+// Exterior trace q+ of face node i of face f: neighbour (local / halo) or boundary ghost.
+template <int NP, int NFP>
+__device__ __forceinline__ void exterior_trace(const StageArgs& A, int code, int nb, int f, int i, const uint8_t* tbl,
+                                               const uint8_t* tblf, const double (&qm)[5], double nx, double ny,
+                                               double nz, double (&qp)[5]) {
+  if (code < CODE_GHOST) {
+    const double* q2 = A.Qin + size_t(nb) * 5 * NP + tbl[(f * 24 + code) * NFP + i];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NP);
+  } else if (code < CODE_BC) {
+    const double* q2 = A.recv + size_t(nb) * 5 * NFP + tblf[(f * 24 + code - CODE_GHOST) * NFP + i];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NFP);
+  } else {
+    const int tag = code - CODE_BC;
+    if (tag == 1) {  // reflective wall, Eq. 4 read as a mirror (A2)
+      const double mn = qm[1] * nx + qm[2] * ny + qm[3] * nz;
+      qp[0] = qm[0];
+      qp[1] = qm[1] - 2.0 * mn * nx;
+      qp[2] = qm[2] - 2.0 * mn * ny;
+      qp[3] = qm[3] - 2.0 * mn * nz;
+      qp[4] = qm[4];
+    } else if (tag == 2) {  // pass-through: ambient state of Eq. 3
+#pragma unroll
+      for (int c = 0; c < 5; ++c) qp[c] = A.qinf[c];
+    } else {  // inflow, Eqs. 5-7
+      inflow_state(A.t, A.inflow_alpha, A.gamma, qp);
+    }
+  }
+}
+
+struct SideFlux {
+  double f[5];   // n.F(q) with the ambient pressure subtracted (A14)
+  double speed;  // |u.n| + c
+};
+
+__device__ __forceinline__ SideFlux side_flux(const double (&q)[5], double nx, double ny, double nz, double gamma,
+                                              double pref) {
+  SideFlux s;
+  const double ri = 1.0 / q[0];
+  const double un = (q[1] * nx + q[2] * ny + q[3] * nz) * ri;
+  const double p = (gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) * ri);
+  const double pd = p - pref;
+  s.f[0] = q[0] * un;
+  s.f[1] = fma(pd, nx, q[1] * un);
+  s.f[2] = fma(pd, ny, q[2] * un);
+  s.f[3] = fma(pd, nz, q[3] * un);
+  s.f[4] = (q[4] + p) * un;
+  s.speed = fabs(un) + sqrt(gamma * p * ri);
+  return s;
+}
+
+// ---------------------------------------------------------------- lock-step kernel (N = 5, 6)
+template <int N>
+struct Tile {
+  static constexpr int EB = (N <= 3) ? 32 : (N == 4 ? 16 : 8);
+  static constexpr int NT = 512;
+  static constexpr int ROWS = (5 * EB + 15) / 16 * 16;
+  static constexpr int MT = ROWS / 16;
+  static constexpr bool OP_SMEM = Shape<N>::OPN * 8 <= 72 * 1024;
+  static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;
+  static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
+  static constexpr int ITEMS = MT * NGRP;
+  static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
+  static constexpr size_t SMEM_OP = OP_SMEM ? size_t(Shape<N>::OPN) * 8 : 0;
+  static constexpr size_t SMEM_Q = size_t(EB) * 5 * Shape<N>::NP * 8;
+  static constexpr size_t SMEM_G = size_t(EB) * GEO * 8;
+  static constexpr size_t SMEM_L = size_t(EB) * 4 * Shape<N>::NFP * 8;
+  static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
+  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_Q + SMEM_G + SMEM_L + SMEM_T;
+  static_assert(SMEM <= 227 * 1024, "tile does not fit in shared memory");
+};
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A) {
   using S = Shape<N>;
@@ -132,7 +217,6 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
   const int tid = threadIdx.x;
   const double* __restrict__ Op = T::OP_SMEM ? sOp : A.op;
 
-  // one-time: operator, tables, zero the padding columns of X
   if (T::OP_SMEM)
     for (int i = tid; i < S::OPN; i += NT) sOp[i] = A.op[i];
   for (int i = tid; i < 96 * NFP; i += NT) {
@@ -148,7 +232,6 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
     const int e0 = A.e_begin + tile * EB;
     const int ne = min(EB, A.e_end - e0);
     __syncthreads();  // previous tile fully consumed
-    // ---------------- A: load state + geometry (contiguous blocks)
     {
       const double* src = A.Qin + size_t(e0) * 5 * NP;
       const int n = ne * 5 * NP;
@@ -158,42 +241,10 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
       for (int i = tid; i < ne * GEO; i += NT) sG[i] = __ldg(g + i);
     }
     __syncthreads();
-    // ---------------- B: volume fluxes -> X[:, 0:3Np)
-    for (int idx = tid; idx < EB * NP; idx += NT) {
+    for (int idx = tid; idx < ne * NP; idx += NT) {
       const int e = idx / NP, n = idx - e * NP;
-      double* xr = sX + (e * 5) * XS;
-      if (e >= ne) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) {
-          xr[f * XS + n] = 0.0;
-          xr[f * XS + NP + n] = 0.0;
-          xr[f * XS + 2 * NP + n] = 0.0;
-        }
-        continue;
-      }
-      const double* q = sQ + e * 5 * NP + n;
-      const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
-      const double ri = 1.0 / rho;
-      const double u = mx * ri, v = my * ri, w = mz * ri;
-      const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-      if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(A.flag, A.gid[e0 + e]);
-      const double* G = sG + e * GEO;
-      const double Ep = E + p;
-      const double pd = p - A.pref;   // background-flux subtraction (A14)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
-        // contravariant velocity and flux along xi_d
-        const double U = cx * u + cy * v + cz * w;
-        double* xc = xr + d * NP + n;
-        xc[0] = rho * U;
-        xc[XS] = mx * U + cx * pd;
-        xc[2 * XS] = my * U + cy * pd;
-        xc[3 * XS] = mz * U + cz * pd;
-        xc[4 * XS] = Ep * U;
-      }
+      volume_node<NP, XS>(sQ + e * 5 * NP + n, sG + e * GEO, sX + (e * 5) * XS + n, gm1, A.pref, A.flag, A.gid[e0 + e]);
     }
-    // ---------------- C: face fluxes -> X[:, 3Np:3Np+4Nfp)
     constexpr int FN = EB * 4 * NFP;
     constexpr int FR = (FN + NT - 1) / NT;
     double qm[FR][5], qp[FR][5];
@@ -206,54 +257,15 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
         sL[idx] = 0.0;
         continue;
       }
-      const int vm = sFm[fi];
-      const double* q = sQ + e * 5 * NP + vm;
+      const double* q = sQ + e * 5 * NP + sFm[fi];
 #pragma unroll
       for (int c = 0; c < 5; ++c) qm[r][c] = q[c * NP];
       const int ke = e0 + e;
-      const int code = A.code[ke * 4 + f];
       const double* G = sG + e * GEO + 9 + 4 * f;
-      const double nx = G[0], ny = G[1], nz = G[2];
-      if (code < CODE_GHOST) {
-        const int k2 = A.nbr[ke * 4 + f];
-        const int node = sTbl[(f * 24 + code) * NFP + i];
-        const double* q2 = A.Qin + size_t(k2) * 5 * NP + node;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[r][c] = __ldg(q2 + c * NP);
-      } else if (code < CODE_BC) {
-        const int g = A.nbr[ke * 4 + f];
-        const int j = sTblf[(f * 24 + code - CODE_GHOST) * NFP + i];
-        const double* q2 = A.recv + size_t(g) * 5 * NFP + j;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[r][c] = __ldg(q2 + c * NFP);
-      } else {
-        const int tag = code - CODE_BC;
-        if (tag == 1) {  // reflective wall, Eq. 4 read as a mirror (A2)
-          const double mn = qm[r][1] * nx + qm[r][2] * ny + qm[r][3] * nz;
-          qp[r][0] = qm[r][0];
-          qp[r][1] = qm[r][1] - 2.0 * mn * nx;
-          qp[r][2] = qm[r][2] - 2.0 * mn * ny;
-          qp[r][3] = qm[r][3] - 2.0 * mn * nz;
-          qp[r][4] = qm[r][4];
-        } else if (tag == 2) {  // pass-through: ambient state of Eq. 3
-#pragma unroll
-          for (int c = 0; c < 5; ++c) qp[r][c] = A.qinf[c];
-        } else {  // inflow, Eqs. 5-7
-          double qi[5];
-          inflow_state(A.t, A.inflow_alpha, gamma, qi);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) qp[r][c] = qi[c];
-        }
-      }
-      // wave speeds |u.n| + c on both sides
-      const double rim = 1.0 / qm[r][0], rip = 1.0 / qp[r][0];
-      const double unm = (qm[r][1] * nx + qm[r][2] * ny + qm[r][3] * nz) * rim;
-      const double unp = (qp[r][1] * nx + qp[r][2] * ny + qp[r][3] * nz) * rip;
-      const double pm = gm1 * (qm[r][4] - 0.5 * (qm[r][1] * qm[r][1] + qm[r][2] * qm[r][2] + qm[r][3] * qm[r][3]) * rim);
-      const double pp = gm1 * (qp[r][4] - 0.5 * (qp[r][1] * qp[r][1] + qp[r][2] * qp[r][2] + qp[r][3] * qp[r][3]) * rip);
-      const double lm = fabs(unm) + sqrt(gamma * pm * rim);
-      const double lp = fabs(unp) + sqrt(gamma * pp * rip);
-      sL[idx] = fmax(lm, lp);
+      exterior_trace<NP, NFP>(A, A.code[ke * 4 + f], A.nbr[ke * 4 + f], f, i, sTbl, sTblf, qm[r], G[0], G[1], G[2], qp[r]);
+      const SideFlux sm = side_flux(qm[r], G[0], G[1], G[2], gamma, A.pref);
+      const SideFlux sp = side_flux(qp[r], G[0], G[1], G[2], gamma, A.pref);
+      sL[idx] = fmax(sm.speed, sp.speed);
     }
     __syncthreads();
 #pragma unroll
@@ -261,12 +273,8 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
       const int idx = tid + r * NT;
       if (idx >= FN) continue;
       const int e = idx / (4 * NFP), fi = idx - e * 4 * NFP, f = fi / NFP;
-      double* xd = sX + (e * 5) * XS + S::KV + fi;
-      if (e >= ne) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) xd[c * XS] = 0.0;
-        continue;
-      }
+      double* xd = sX + (e * 5) * XS + S::KVP + fi;
+      if (e >= ne) continue;
       double lam;
       if (A.lambda_mode == 0) {
         const double* l = sL + e * 4 * NFP + f * NFP;
@@ -277,40 +285,15 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
         lam = sL[idx];
       }
       const double* G = sG + e * GEO + 9 + 4 * f;
-      const double nx = G[0], ny = G[1], nz = G[2], fs = G[3];
-      // normal fluxes n.F(q) on both sides
-      double fm[5], fp[5];
-      {
-        const double ri = 1.0 / qm[r][0];
-        const double un = (qm[r][1] * nx + qm[r][2] * ny + qm[r][3] * nz) * ri;
-        const double p = gm1 * (qm[r][4] - 0.5 * (qm[r][1] * qm[r][1] + qm[r][2] * qm[r][2] + qm[r][3] * qm[r][3]) * ri);
-        const double pd = p - A.pref;
-        fm[0] = qm[r][0] * un;
-        fm[1] = qm[r][1] * un + pd * nx;
-        fm[2] = qm[r][2] * un + pd * ny;
-        fm[3] = qm[r][3] * un + pd * nz;
-        fm[4] = (qm[r][4] + p) * un;
-      }
-      {
-        const double ri = 1.0 / qp[r][0];
-        const double un = (qp[r][1] * nx + qp[r][2] * ny + qp[r][3] * nz) * ri;
-        const double p = gm1 * (qp[r][4] - 0.5 * (qp[r][1] * qp[r][1] + qp[r][2] * qp[r][2] + qp[r][3] * qp[r][3]) * ri);
-        const double pd = p - A.pref;
-        fp[0] = qp[r][0] * un;
-        fp[1] = qp[r][1] * un + pd * nx;
-        fp[2] = qp[r][2] * un + pd * ny;
-        fp[3] = qp[r][3] * un + pd * nz;
-        fp[4] = (qp[r][4] + p) * un;
-      }
-      // dF = Fscale (n.F(q-) - F*),  F* = 1/2 (fm + fp) - 1/2 lam (q+ - q-)
+      const SideFlux sm = side_flux(qm[r], G[0], G[1], G[2], gamma, A.pref);
+      const SideFlux sp = side_flux(qp[r], G[0], G[1], G[2], gamma, A.pref);
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
-        const double fstar = 0.5 * (fm[c] + fp[c]) - 0.5 * lam * (qp[r][c] - qm[r][c]);
-        xd[c * XS] = fs * (fm[c] - fstar);
+        const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[r][c] - qm[r][c]);
+        xd[c * XS] = G[3] * (sm.f[c] - fstar);
       }
     }
     __syncthreads();
-    // ---------------- D + E: DMMA contraction and epilogue
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     for (int item = warp; item < T::ITEMS; item += NT / 32) {
       const int mt = item / T::NGRP, ng = item - mt * T::NGRP;
@@ -328,7 +311,6 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
           if (nt < S::NTL) dmma_16x8x4(acc[j], a0, a1, ob[(ks * S::NTL + nt) * 32]);
         }
       }
-      // epilogue: rows (mt*16 + g, +8), cols nt*8 + 2*t4 + {0,1}
 #pragma unroll
       for (int j = 0; j < T::NTG; ++j) {
         const int nt = ng * T::NTG + j;
@@ -354,6 +336,245 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
           }
         }
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- warp-specialised kernel (N <= 4)
+template <int N>
+struct WS {
+  static constexpr int EB = (N <= 3) ? 32 : 16;
+  static constexpr int PW = 8, CW = 8;                      // producer / consumer warps
+  static constexpr int NT = 32 * (PW + CW);
+  static constexpr int ROWS = 5 * EB;                       // multiple of 16
+  static constexpr int MT = ROWS / 16;
+  static_assert(ROWS % 16 == 0, "rows must fill DMMA m16 tiles");
+  // consumer work items: (m-tile, group of NTG n-tiles); a consumer warp owns up to IPW items
+  static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;
+  static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
+  static constexpr int ITEMS = MT * NGRP;
+  static constexpr int IPW = (ITEMS + CW - 1) / CW;
+  static constexpr int NSEG = 32 / Shape<N>::NFP;           // faces per producer warp-pass
+  static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
+  static constexpr size_t SMEM_OP = size_t(Shape<N>::OPN) * 8;
+  static constexpr size_t SMEM_Q = size_t(2) * EB * 5 * Shape<N>::NP * 8;
+  static constexpr size_t SMEM_G = size_t(2) * EB * GEO * 8;
+  static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
+  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_Q + SMEM_G + SMEM_T;
+  static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
+  // named barriers
+  static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5, BAR_Q_EMPTY = 6;
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs A) {
+  using S = Shape<N>;
+  using W = WS<N>;
+  constexpr int NP = S::NP, NFP = S::NFP, EB = W::EB, XS = S::XS, NT = W::NT;
+  constexpr int PT = 32 * W::PW;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sX = reinterpret_cast<double*>(smem);
+  double* sOp = sX + W::ROWS * XS;
+  double* sQ = sOp + S::OPN;               // [2][EB][5][NP]
+  double* sG = sQ + 2 * EB * 5 * NP;       // [2][EB][GEO]
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sG + 2 * EB * GEO);
+  uint8_t* sTblf = sTbl + 96 * NFP;
+  uint8_t* sFm = sTblf + 96 * NFP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int i = tid; i < S::OPN; i += NT) sOp[i] = A.op[i];
+  for (int i = tid; i < 96 * NFP; i += NT) {
+    sTbl[i] = A.tbl[i];
+    sTblf[i] = A.tblf[i];
+  }
+  for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
+  for (int i = tid; i < W::ROWS * XS; i += NT) sX[i] = 0.0;   // padding columns stay 0
+  __syncthreads();
+
+  const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
+  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp < W::PW) {
+    // ======================= producers: load, volume flux, face flux
+    const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+    for (int j = 0; j < nmine; ++j) {
+      const int tile = blockIdx.x + j * gridDim.x;
+      const int e0 = A.e_begin + tile * EB;
+      const int ne = min(EB, A.e_end - e0);
+      const int buf = j & 1;
+      double* q_s = sQ + buf * EB * 5 * NP;
+      double* g_s = sG + buf * EB * GEO;
+      if (j >= 2) nbar_sync(W::BAR_Q_EMPTY + buf, NT);   // consumers done with tile j-2's Q
+      {
+        const double2* src = reinterpret_cast<const double2*>(A.Qin + size_t(e0) * 5 * NP);
+        double2* dst = reinterpret_cast<double2*>(q_s);
+        const int n2 = ne * 5 * NP / 2;                     // EB even, 5*NP*EB even
+        for (int i = tid; i < n2; i += PT) dst[i] = __ldg(src + i);
+        if (ne & 1) {
+          if (tid == 0) q_s[ne * 5 * NP - 1] = __ldg(A.Qin + size_t(e0) * 5 * NP + ne * 5 * NP - 1);
+        }
+        for (int i = ne * 5 * NP + tid; i < EB * 5 * NP; i += PT) q_s[i] = 0.0;
+        const double* gsrc = A.geo + size_t(e0) * GEO;
+        for (int i = tid; i < ne * GEO; i += PT) g_s[i] = __ldg(gsrc + i);
+      }
+      nbar_sync(W::BAR_P, PT);
+      // ---- volume fluxes -> X[:, 0:3NP)
+      if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
+      for (int idx = tid; idx < EB * NP; idx += PT) {
+        const int e = idx / NP, n = idx - e * NP;
+        double* xr = sX + (e * 5) * XS + n;
+        if (e < ne) {
+          volume_node<NP, XS>(q_s + e * 5 * NP + n, g_s + e * GEO, xr, gm1, A.pref, A.flag, A.gid[e0 + e]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            xr[c * XS] = 0.0;
+            xr[c * XS + NP] = 0.0;
+            xr[c * XS + 2 * NP] = 0.0;
+          }
+        }
+      }
+      nbar_arrive(W::BAR_XV_FULL, NT);
+      // ---- face fluxes -> X[:, KVP:KVP+4NFP): one face per NFP-lane segment
+      if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
+      const int seg = lane / NFP, i = lane - seg * NFP;
+      const bool lane_ok = seg < W::NSEG;
+      for (int fb = warp * W::NSEG; fb < EB * 4; fb += W::PW * W::NSEG) {
+        const int face = fb + seg;
+        const int e = face >> 2, f = face & 3;
+        const bool act = lane_ok && face < EB * 4 && e < ne;
+        double qm[5], qp[5];
+        double nx = 0, ny = 0, nz = 1, fs = 0, lam = 0;
+        SideFlux sm, sp;
+        if (act) {
+          const double* G = g_s + e * GEO + 9 + 4 * f;
+          nx = G[0]; ny = G[1]; nz = G[2]; fs = G[3];
+          const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+          const int ke = e0 + e;
+          exterior_trace<NP, NFP>(A, A.code[ke * 4 + f], A.nbr[ke * 4 + f], f, i, sTbl, sTblf, qm, nx, ny, nz, qp);
+          sm = side_flux(qm, nx, ny, nz, gamma, A.pref);
+          sp = side_flux(qp, nx, ny, nz, gamma, A.pref);
+          lam = fmax(sm.speed, sp.speed);
+        }
+        if (A.lambda_mode == 0) {
+          // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
+          const int base = seg * NFP;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, lam, d);
+            if (lane_ok && i >= d) lam = fmax(lam, o);
+          }
+          const double m = __shfl_sync(0xffffffffu, lam, lane_ok ? base + NFP - 1 : lane);
+          lam = m;
+        }
+        if (act) {
+          double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[c] - qm[c]);
+            xd[c * XS] = fs * (sm.f[c] - fstar);
+          }
+        } else if (lane_ok && face < EB * 4 && e >= ne) {
+          double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) xd[c * XS] = 0.0;
+        }
+      }
+      nbar_arrive(W::BAR_XF_FULL, NT);
+    }
+  } else {
+    // ======================= consumers: DMMA contraction + LSERK epilogue
+    const int cw = warp - W::PW, g = lane >> 2, t4 = lane & 3;
+    int mt[W::IPW], ng[W::IPW];
+    bool on[W::IPW];
+#pragma unroll
+    for (int it = 0; it < W::IPW; ++it) {
+      const int item = cw + it * W::CW;
+      on[it] = item < W::ITEMS;
+      mt[it] = on[it] ? item / W::NGRP : 0;
+      ng[it] = on[it] ? item - mt[it] * W::NGRP : 0;
+    }
+    for (int j = 0; j < nmine; ++j) {
+      const int tile = blockIdx.x + j * gridDim.x;
+      const int e0 = A.e_begin + tile * EB;
+      const int ne = min(EB, A.e_end - e0);
+      const int buf = j & 1;
+      const double* q_s = sQ + buf * EB * 5 * NP;
+      double acc[W::IPW][W::NTG][4];
+#pragma unroll
+      for (int it = 0; it < W::IPW; ++it)
+#pragma unroll
+        for (int jj = 0; jj < W::NTG; ++jj) acc[it][jj][0] = acc[it][jj][1] = acc[it][jj][2] = acc[it][jj][3] = 0.0;
+      auto kloop = [&](int k0, int k1) {
+#pragma unroll 2
+        for (int ks = k0; ks < k1; ++ks) {
+#pragma unroll
+          for (int it = 0; it < W::IPW; ++it) {
+            if (!on[it]) continue;
+            const double* xa = sX + (mt[it] * 16 + g) * XS + t4 + ks * 4;
+            const double a0 = xa[0], a1 = xa[8 * XS];
+#pragma unroll
+            for (int jj = 0; jj < W::NTG; ++jj) {
+              const int nt = ng[it] * W::NTG + jj;
+              if (nt < S::NTL) dmma_16x8x4(acc[it][jj], a0, a1, sOp[(ks * S::NTL + nt) * 32 + lane]);
+            }
+          }
+        }
+      };
+      nbar_sync(W::BAR_XV_FULL, NT);
+      kloop(0, S::KSV);
+      if (j + 1 < nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+      // prefetch the residual while the face half of X is produced
+      double rprev[W::IPW][W::NTG][4];
+#pragma unroll
+      for (int it = 0; it < W::IPW; ++it)
+#pragma unroll
+        for (int jj = 0; jj < W::NTG; ++jj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int row = mt[it] * 16 + g + 8 * h, e = row / 5, c = row - 5 * (row / 5);
+              const int n = (ng[it] * W::NTG + jj) * 8 + 2 * t4 + q;
+              const bool ok = MODE == MODE_UPDATE && on[it] && e < ne && n < NP && (ng[it] * W::NTG + jj) < S::NTL;
+              rprev[it][jj][2 * h + q] = ok ? __ldg(A.res + (size_t(e0 + e) * 5 + c) * NP + n) : 0.0;
+            }
+      nbar_sync(W::BAR_XF_FULL, NT);
+      kloop(S::KSV, S::KS4);
+      if (j + 1 < nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
+#pragma unroll
+      for (int it = 0; it < W::IPW; ++it) {
+        if (!on[it]) continue;
+#pragma unroll
+        for (int jj = 0; jj < W::NTG; ++jj) {
+          const int nt = ng[it] * W::NTG + jj;
+          if (nt >= S::NTL) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = mt[it] * 16 + g + 8 * h;
+            const int e = row / 5, c = row - 5 * (row / 5);
+            if (e >= ne) continue;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int n = nt * 8 + 2 * t4 + q;
+              if (n >= NP) continue;
+              const double rhs = acc[it][jj][2 * h + q];
+              if (MODE == MODE_UPDATE) {
+                const size_t gi = (size_t(e0 + e) * 5 + c) * NP + n;
+                const double rr = fma(A.a, rprev[it][jj][2 * h + q], A.dt * rhs);
+                A.res[gi] = rr;
+                A.Qout[gi] = fma(A.b, rr, q_s[(e * 5 + c) * NP + n]);
+              } else {
+                A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
+              }
+            }
+          }
+        }
+      }
+      if (j + 2 < nmine) nbar_arrive(W::BAR_Q_EMPTY + buf, NT);
     }
   }
 }

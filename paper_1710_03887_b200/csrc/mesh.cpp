@@ -334,15 +334,18 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
         }
   }
 
-  // ---- DMMA B-fragment operator: Op = [-Dr -Ds -Dt LIFT] (Np x KT), B[k][n] = Op[n][k]
-  const int KT = 3 * Np + 4 * Nfp, KPAD = (KT + 3) / 4 * 4, NPAD = (Np + 7) / 8 * 8;
+  // ---- DMMA B-fragment operator: Op = [-Dr -Ds -Dt 0 LIFT] (Np x KPAD), B[k][n] = Op[n][k];
+  // the volume block is padded to a multiple of 4 columns (KVP) so the DMMA k-steps of
+  // the volume and face halves of X never straddle (kernels.cuh Shape<N>)
+  const int KV = 3 * Np, KVP = (KV + 3) / 4 * 4, KPAD = KVP + 4 * Nfp, NPAD = (Np + 7) / 8 * 8;
   const int KS4 = KPAD / 4, NTL = NPAD / 8;
   auto op = [&](int n, int k) -> double {
-    if (n >= Np || k >= KT) return 0.0;
+    if (n >= Np || k >= KPAD) return 0.0;
     if (k < Np) return -c->ref.Dr[n * Np + k];
     if (k < 2 * Np) return -c->ref.Ds[n * Np + k - Np];
     if (k < 3 * Np) return -c->ref.Dt[n * Np + k - 2 * Np];
-    return c->ref.LIFT[n * 4 * Nfp + (k - 3 * Np)];
+    if (k < KVP) return 0.0;
+    return c->ref.LIFT[n * 4 * Nfp + (k - KVP)];
   };
   c->opfrag.assign(size_t(KS4) * NTL * 32, 0.0);
   for (int ks = 0; ks < KS4; ++ks)
