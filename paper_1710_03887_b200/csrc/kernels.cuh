@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
   using S = Shape<N>;
   using T = Tile<N>;
   constexpr int NP = S::NP, NFP = S::NFP, EB = T::EB, NT = T::NT, XS = S::XS;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   double* sX = reinterpret_cast<double*>(smem);
   double* sOp = sX + T::ROWS * XS;
   double* sQ = sOp + (T::OP_SMEM ? S::OPN : 0);
@@ -341,6 +341,29 @@ __global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A
 }
 
 // ---------------------------------------------------------------- warp-specialised kernel (N <= 4)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// TMA 1D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0, 16B aligned)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 template <int N>
 struct WS {
   static constexpr int EB = (N <= 3) ? 32 : 16;
@@ -352,15 +375,22 @@ struct WS {
   // consumer work items: (m-tile, group of NTG n-tiles); a consumer warp owns up to IPW items
   static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;
   static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
+  static constexpr int NTLP = NGRP * NTG;                   // n-tiles incl. a zero pad to fill groups
   static constexpr int ITEMS = MT * NGRP;
   static constexpr int IPW = (ITEMS + CW - 1) / CW;
   static constexpr int NSEG = 32 / Shape<N>::NFP;           // faces per producer warp-pass
+  static constexpr int OPS = Shape<N>::KS4 * NTLP * 32;     // doubles of the grouped B operand
+  // per-buffer bytes of the TMA-loaded tile inputs
+  static constexpr uint32_t BQ = uint32_t(EB) * 5 * Shape<N>::NP * 8;
+  static constexpr uint32_t BG = uint32_t(EB) * GEO * 8;
+  static constexpr uint32_t BN = uint32_t(EB) * 4 * 4;
+  static constexpr uint32_t BC = uint32_t(EB) * 4;
+  static_assert(BQ % 16 == 0 && BG % 16 == 0 && BN % 16 == 0 && BC % 16 == 0, "TMA sizes");
   static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
-  static constexpr size_t SMEM_OP = size_t(Shape<N>::OPN) * 8;
-  static constexpr size_t SMEM_Q = size_t(2) * EB * 5 * Shape<N>::NP * 8;
-  static constexpr size_t SMEM_G = size_t(2) * EB * GEO * 8;
+  static constexpr size_t SMEM_OP = size_t(OPS) * 8;
+  static constexpr size_t SMEM_IN = size_t(2) * (BQ + BG + BN + BC);
   static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_Q + SMEM_G + SMEM_T;
+  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_IN + SMEM_T + 16;
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
   static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5, BAR_Q_EMPTY = 6;
@@ -372,23 +402,40 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   using W = WS<N>;
   constexpr int NP = S::NP, NFP = S::NFP, EB = W::EB, XS = S::XS, NT = W::NT;
   constexpr int PT = 32 * W::PW;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   double* sX = reinterpret_cast<double*>(smem);
   double* sOp = sX + W::ROWS * XS;
-  double* sQ = sOp + S::OPN;               // [2][EB][5][NP]
-  double* sG = sQ + 2 * EB * 5 * NP;       // [2][EB][GEO]
-  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sG + 2 * EB * GEO);
+  unsigned char* in0 = reinterpret_cast<unsigned char*>(sOp + W::OPS);
+  // per buffer b: Q | geo | nbr | code
+  auto bufQ = [&](int b) { return reinterpret_cast<double*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC)); };
+  auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ); };
+  auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ + W::BG); };
+  auto bufC = [&](int b) {
+    return reinterpret_cast<uint8_t*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ + W::BG + W::BN);
+  };
+  uint8_t* sTbl = in0 + 2 * (W::BQ + W::BG + W::BN + W::BC);
   uint8_t* sTblf = sTbl + 96 * NFP;
   uint8_t* sFm = sTblf + 96 * NFP;
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int i = tid; i < S::OPN; i += NT) sOp[i] = A.op[i];
+  // B operand regrouped per (k-step, n-tile group): lane reads its NTG values contiguously
+  for (int i = tid; i < W::OPS; i += NT) {
+    const int l = i % (32 * W::NTG), rest = i / (32 * W::NTG);
+    const int grp = rest % W::NGRP, ks = rest / W::NGRP;
+    const int ln = l / W::NTG, jj = l % W::NTG, nt = grp * W::NTG + jj;
+    sOp[i] = nt < S::NTL ? A.op[(ks * S::NTL + nt) * 32 + ln] : 0.0;
+  }
   for (int i = tid; i < 96 * NFP; i += NT) {
     sTbl[i] = A.tbl[i];
     sTblf[i] = A.tblf[i];
   }
   for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
   for (int i = tid; i < W::ROWS * XS; i += NT) sX[i] = 0.0;   // padding columns stay 0
+  if (tid == 0) {
+    mbar_init(&sBar[0], 1);
+    mbar_init(&sBar[1], 1);
+  }
   __syncthreads();
 
   const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
@@ -396,29 +443,48 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (warp < W::PW) {
-    // ======================= producers: load, volume flux, face flux
+    // ======================= producers: load (TMA), volume flux, face flux
     const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+    // inputs of local tile jj into buffer jj&1: TMA bulk copies for a full tile, plain loads otherwise
+    auto fetch = [&](int jj) {
+      const int tile = blockIdx.x + jj * gridDim.x;
+      const int e0 = A.e_begin + tile * EB;
+      const int ne = min(EB, A.e_end - e0);
+      const int b = jj & 1;
+      if (ne == EB) {
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&sBar[b], W::BQ + W::BG + W::BN + W::BC);
+          tma_load_1d(bufQ(b), A.Qin + size_t(e0) * 5 * NP, W::BQ, &sBar[b]);
+          tma_load_1d(bufG(b), A.geo + size_t(e0) * GEO, W::BG, &sBar[b]);
+          tma_load_1d(bufN(b), A.nbr + size_t(e0) * 4, W::BN, &sBar[b]);
+          tma_load_1d(bufC(b), A.code + size_t(e0) * 4, W::BC, &sBar[b]);
+        }
+      } else {
+        double* q_s = bufQ(b);
+        double* g_s = bufG(b);
+        int* n_s = bufN(b);
+        uint8_t* c_s = bufC(b);
+        for (int i = tid; i < EB * 5 * NP; i += PT) q_s[i] = i < ne * 5 * NP ? __ldg(A.Qin + size_t(e0) * 5 * NP + i) : 0.0;
+        for (int i = tid; i < EB * GEO; i += PT) g_s[i] = i < ne * GEO ? __ldg(A.geo + size_t(e0) * GEO + i) : 0.0;
+        for (int i = tid; i < EB * 4; i += PT) {
+          n_s[i] = i < ne * 4 ? __ldg(A.nbr + size_t(e0) * 4 + i) : 0;
+          c_s[i] = i < ne * 4 ? A.code[size_t(e0) * 4 + i] : uint8_t(CODE_BC + 2);
+        }
+        nbar_sync(W::BAR_P, PT);
+      }
+    };
+    if (nmine > 0) fetch(0);
     for (int j = 0; j < nmine; ++j) {
       const int tile = blockIdx.x + j * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
       const int ne = min(EB, A.e_end - e0);
       const int buf = j & 1;
-      double* q_s = sQ + buf * EB * 5 * NP;
-      double* g_s = sG + buf * EB * GEO;
-      if (j >= 2) nbar_sync(W::BAR_Q_EMPTY + buf, NT);   // consumers done with tile j-2's Q
-      {
-        const double2* src = reinterpret_cast<const double2*>(A.Qin + size_t(e0) * 5 * NP);
-        double2* dst = reinterpret_cast<double2*>(q_s);
-        const int n2 = ne * 5 * NP / 2;                     // EB even, 5*NP*EB even
-        for (int i = tid; i < n2; i += PT) dst[i] = __ldg(src + i);
-        if (ne & 1) {
-          if (tid == 0) q_s[ne * 5 * NP - 1] = __ldg(A.Qin + size_t(e0) * 5 * NP + ne * 5 * NP - 1);
-        }
-        for (int i = ne * 5 * NP + tid; i < EB * 5 * NP; i += PT) q_s[i] = 0.0;
-        const double* gsrc = A.geo + size_t(e0) * GEO;
-        for (int i = tid; i < ne * GEO; i += PT) g_s[i] = __ldg(gsrc + i);
-      }
-      nbar_sync(W::BAR_P, PT);
+      const double* q_s = bufQ(buf);
+      const double* g_s = bufG(buf);
+      const int* n_s = bufN(buf);
+      const uint8_t* c_s = bufC(buf);
+      if (ne == EB) mbar_wait(&sBar[buf], (j >> 1) & 1);
       // ---- volume fluxes -> X[:, 0:3NP)
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       for (int idx = tid; idx < EB * NP; idx += PT) {
@@ -436,51 +502,67 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         }
       }
       nbar_arrive(W::BAR_XV_FULL, NT);
-      // ---- face fluxes -> X[:, KVP:KVP+4NFP): one face per NFP-lane segment
+      // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1)
+      if (j + 1 < nmine) {
+        if (j + 1 >= 2) nbar_sync(W::BAR_Q_EMPTY + ((j + 1) & 1), NT);
+        fetch(j + 1);
+      }
+      // ---- face fluxes -> X[:, KVP:KVP+4NFP): one face per NFP-lane segment, two passes at a time
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
       const int seg = lane / NFP, i = lane - seg * NFP;
       const bool lane_ok = seg < W::NSEG;
-      for (int fb = warp * W::NSEG; fb < EB * 4; fb += W::PW * W::NSEG) {
-        const int face = fb + seg;
-        const int e = face >> 2, f = face & 3;
-        const bool act = lane_ok && face < EB * 4 && e < ne;
-        double qm[5], qp[5];
-        double nx = 0, ny = 0, nz = 1, fs = 0, lam = 0;
-        SideFlux sm, sp;
-        if (act) {
-          const double* G = g_s + e * GEO + 9 + 4 * f;
-          nx = G[0]; ny = G[1]; nz = G[2]; fs = G[3];
-          const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+      constexpr int STRIDE = W::PW * W::NSEG;
+      for (int fb = warp * W::NSEG; fb < EB * 4; fb += 2 * STRIDE) {
+        double qm[2][5], qp[2][5], nv[2][4];
+        bool act[2];
 #pragma unroll
-          for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
-          const int ke = e0 + e;
-          exterior_trace<NP, NFP>(A, A.code[ke * 4 + f], A.nbr[ke * 4 + f], f, i, sTbl, sTblf, qm, nx, ny, nz, qp);
-          sm = side_flux(qm, nx, ny, nz, gamma, A.pref);
-          sp = side_flux(qp, nx, ny, nz, gamma, A.pref);
-          lam = fmax(sm.speed, sp.speed);
-        }
-        if (A.lambda_mode == 0) {
-          // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
-          const int base = seg * NFP;
+        for (int u = 0; u < 2; ++u) {
+          const int face = fb + u * STRIDE + seg;
+          const int e = face >> 2, f = face & 3;
+          act[u] = lane_ok && face < EB * 4 && e < ne;
+          if (act[u]) {
+            const double* G = g_s + e * GEO + 9 + 4 * f;
+            nv[u][0] = G[0]; nv[u][1] = G[1]; nv[u][2] = G[2]; nv[u][3] = G[3];
+            const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
 #pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const double o = __shfl_up_sync(0xffffffffu, lam, d);
-            if (lane_ok && i >= d) lam = fmax(lam, o);
+            for (int c = 0; c < 5; ++c) qm[u][c] = q[c * NP];
+            exterior_trace<NP, NFP>(A, c_s[e * 4 + f], n_s[e * 4 + f], f, i, sTbl, sTblf, qm[u], nv[u][0], nv[u][1],
+                                    nv[u][2], qp[u]);
           }
-          const double m = __shfl_sync(0xffffffffu, lam, lane_ok ? base + NFP - 1 : lane);
-          lam = m;
         }
-        if (act) {
-          double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[c] - qm[c]);
-            xd[c * XS] = fs * (sm.f[c] - fstar);
+        for (int u = 0; u < 2; ++u) {
+          const int face = fb + u * STRIDE + seg;
+          const int e = face >> 2, f = face & 3;
+          if (fb + u * STRIDE >= EB * 4) break;   // warp-uniform
+          double lam = 0.0;
+          SideFlux sm, sp;
+          if (act[u]) {
+            sm = side_flux(qm[u], nv[u][0], nv[u][1], nv[u][2], gamma, A.pref);
+            sp = side_flux(qp[u], nv[u][0], nv[u][1], nv[u][2], gamma, A.pref);
+            lam = fmax(sm.speed, sp.speed);
           }
-        } else if (lane_ok && face < EB * 4 && e >= ne) {
-          double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+          if (A.lambda_mode == 0) {
+            // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
 #pragma unroll
-          for (int c = 0; c < 5; ++c) xd[c * XS] = 0.0;
+            for (int d = 1; d < 32; d <<= 1) {
+              const double o = __shfl_up_sync(0xffffffffu, lam, d);
+              if (lane_ok && i >= d) lam = fmax(lam, o);
+            }
+            lam = __shfl_sync(0xffffffffu, lam, lane_ok ? seg * NFP + NFP - 1 : lane);
+          }
+          if (act[u]) {
+            double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+              const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[u][c] - qm[u][c]);
+              xd[c * XS] = nv[u][3] * (sm.f[c] - fstar);
+            }
+          } else if (lane_ok && face < EB * 4) {
+            double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) xd[c * XS] = 0.0;
+          }
         }
       }
       nbar_arrive(W::BAR_XF_FULL, NT);
@@ -502,24 +584,27 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int e0 = A.e_begin + tile * EB;
       const int ne = min(EB, A.e_end - e0);
       const int buf = j & 1;
-      const double* q_s = sQ + buf * EB * 5 * NP;
+      const double* q_s = bufQ(buf);
       double acc[W::IPW][W::NTG][4];
 #pragma unroll
       for (int it = 0; it < W::IPW; ++it)
 #pragma unroll
         for (int jj = 0; jj < W::NTG; ++jj) acc[it][jj][0] = acc[it][jj][1] = acc[it][jj][2] = acc[it][jj][3] = 0.0;
       auto kloop = [&](int k0, int k1) {
-#pragma unroll 2
+#pragma unroll 4
         for (int ks = k0; ks < k1; ++ks) {
 #pragma unroll
           for (int it = 0; it < W::IPW; ++it) {
             if (!on[it]) continue;
             const double* xa = sX + (mt[it] * 16 + g) * XS + t4 + ks * 4;
             const double a0 = xa[0], a1 = xa[8 * XS];
-#pragma unroll
-            for (int jj = 0; jj < W::NTG; ++jj) {
-              const int nt = ng[it] * W::NTG + jj;
-              if (nt < S::NTL) dmma_16x8x4(acc[it][jj], a0, a1, sOp[(ks * S::NTL + nt) * 32 + lane]);
+            const double* ob = sOp + ((ks * W::NGRP + ng[it]) * 32 + lane) * W::NTG;
+            if constexpr (W::NTG == 2) {
+              const double2 b = *reinterpret_cast<const double2*>(ob);
+              dmma_16x8x4(acc[it][0], a0, a1, b.x);
+              dmma_16x8x4(acc[it][1], a0, a1, b.y);
+            } else {
+              dmma_16x8x4(acc[it][0], a0, a1, ob[0]);
             }
           }
         }
@@ -539,7 +624,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
             for (int q = 0; q < 2; ++q) {
               const int row = mt[it] * 16 + g + 8 * h, e = row / 5, c = row - 5 * (row / 5);
               const int n = (ng[it] * W::NTG + jj) * 8 + 2 * t4 + q;
-              const bool ok = MODE == MODE_UPDATE && on[it] && e < ne && n < NP && (ng[it] * W::NTG + jj) < S::NTL;
+              const bool ok = MODE == MODE_UPDATE && on[it] && e < ne && n < NP;
               rprev[it][jj][2 * h + q] = ok ? __ldg(A.res + (size_t(e0 + e) * 5 + c) * NP + n) : 0.0;
             }
       nbar_sync(W::BAR_XF_FULL, NT);
