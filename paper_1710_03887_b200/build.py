@@ -47,6 +47,11 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
+def defines() -> dict:
+    """Compile-time tuning knobs from the environment (DG_WS_PW=...), for experiments."""
+    return {k: os.environ[k] for k in ("DG_WS_PW", "DG_EPI_TMA") if k in os.environ}
+
+
 def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if not force and up_to_date():
         return LIB
@@ -62,6 +67,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         objs.append(o)
     o = os.path.join(bdir, "api.cu.o")
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+    extra += [f"-D{k}={v}" for k, v in defines().items()]
     _run([NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                           "-c", os.path.join(CSRC, "api.cu"), "-o", o] + inc + extra)
     objs.append(o)

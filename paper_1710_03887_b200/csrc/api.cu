@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -154,6 +155,7 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   for (int i = 0; i < 5; ++i) A.qinf[i] = c->q_inf[i];
   A.inflow_alpha = c->inflow_alpha;
   A.lambda_mode = c->lambda_mode;
+  if (const char* dbg = std::getenv("DG_DEBUG_TIMING")) A.debug = std::atoi(dbg);
   const double* qi = c->q_inf;
   A.pref = (c->gamma - 1.0) * (qi[4] - 0.5 * (qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]) / qi[0]);
   return A;

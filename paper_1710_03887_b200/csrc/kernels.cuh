@@ -56,6 +56,7 @@ struct StageArgs {
   double qinf[5];
   double inflow_alpha;
   int lambda_mode;
+  int debug;              // timing experiments only: 1 = skip DMMA, 2 = skip producer flux math
 };
 
 template <int N>
@@ -102,13 +103,34 @@ __device__ __forceinline__ void inflow_state(double t, double alpha, double gamm
 
 enum { MODE_UPDATE = 0, MODE_RHS = 1 };
 
+// Reciprocal and square root from the MUFU seeds plus two Newton steps each: within
+// ~1 ulp of the correctly rounded results (the parity tests bound the effect), at a
+// third of the issue cost of IEEE div/sqrt with their slow-path branches.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double sqrt_nr(double x) {   // x > 0
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  return x * y;
+}
+
 // ---------------------------------------------------------------- pointwise pieces
 // Volume flux at one node: q -> 15 contravariant flux values in X rows e*5+c, cols d*NP+n.
 template <int NP, int XS>
 __device__ __forceinline__ void volume_node(const double* q, const double* G, double* xr, double gm1, double pref,
                                             int* flag, int64_t gid) {
   const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
-  const double ri = 1.0 / rho;
+  const double ri = rcp_nr(rho);
   const double u = mx * ri, v = my * ri, w = mz * ri;
   const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
   if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(flag, gid);
@@ -166,7 +188,7 @@ struct SideFlux {
 __device__ __forceinline__ SideFlux side_flux(const double (&q)[5], double nx, double ny, double nz, double gamma,
                                               double pref) {
   SideFlux s;
-  const double ri = 1.0 / q[0];
+  const double ri = rcp_nr(q[0]);
   const double un = (q[1] * nx + q[2] * ny + q[3] * nz) * ri;
   const double p = (gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) * ri);
   const double pd = p - pref;
@@ -175,7 +197,7 @@ __device__ __forceinline__ SideFlux side_flux(const double (&q)[5], double nx, d
   s.f[2] = fma(pd, ny, q[2] * un);
   s.f[3] = fma(pd, nz, q[3] * un);
   s.f[4] = (q[4] + p) * un;
-  s.speed = fabs(un) + sqrt(gamma * p * ri);
+  s.speed = fabs(un) + sqrt_nr(gamma * p * ri);
   return s;
 }
 
@@ -364,74 +386,228 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+template <int XSTR_, int K0_, int K1_>
+struct KBlk {
+  static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_;
+};
+
 template <int N>
 struct WS {
-  static constexpr int EB = (N <= 3) ? 32 : 16;
+  static constexpr int EB = (N <= 2) ? 32 : 16;
   static constexpr int PW = 8, CW = 8;                      // producer / consumer warps
   static constexpr int NT = 32 * (PW + CW);
+  static constexpr int PT = 32 * PW, CT = 32 * CW;
   static constexpr int ROWS = 5 * EB;                       // multiple of 16
   static constexpr int MT = ROWS / 16;
   static_assert(ROWS % 16 == 0, "rows must fill DMMA m16 tiles");
-  // consumer work items: (m-tile, group of NTG n-tiles); a consumer warp owns up to IPW items
-  static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;
-  static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
-  static constexpr int NTLP = NGRP * NTG;                   // n-tiles incl. a zero pad to fill groups
-  static constexpr int ITEMS = MT * NGRP;
-  static constexpr int IPW = (ITEMS + CW - 1) / CW;
+  // consumer work items: (m-tile, group of <= NTG n-tiles); a consumer warp owns up to IPW items
+  static constexpr int NTG = 2;                             // B operand stored as n-tile pairs (+ odd tail)
   static constexpr int NSEG = 32 / Shape<N>::NFP;           // faces per producer warp-pass
-  static constexpr int OPS = Shape<N>::KS4 * NTLP * 32;     // doubles of the grouped B operand
+  // X is split into its volume block [ROWS][XSV] and face block [ROWS][XSF];
+  // strides == 12 (mod 16) doubles keep the A-fragment loads conflict-free
+  static constexpr int XSV = (Shape<N>::KVP + 3) / 16 * 16 + 12;
+  static constexpr int XSF = (4 * Shape<N>::NFP + 3) / 16 * 16 + 12;
   // per-buffer bytes of the TMA-loaded tile inputs
   static constexpr uint32_t BQ = uint32_t(EB) * 5 * Shape<N>::NP * 8;
   static constexpr uint32_t BG = uint32_t(EB) * GEO * 8;
   static constexpr uint32_t BN = uint32_t(EB) * 4 * 4;
   static constexpr uint32_t BC = uint32_t(EB) * 4;
+  static constexpr uint32_t BIN = BQ + BG + BN + BC;
   static_assert(BQ % 16 == 0 && BG % 16 == 0 && BN % 16 == 0 && BC % 16 == 0, "TMA sizes");
-  static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
-  static constexpr size_t SMEM_OP = size_t(OPS) * 8;
-  static constexpr size_t SMEM_IN = size_t(2) * (BQ + BG + BN + BC);
+  static_assert(size_t(ROWS) * XSF >= size_t(EB) * 5 * Shape<N>::NP, "face block doubles as the residual staging tile");
+  static constexpr size_t SMEM_XV = size_t(ROWS) * XSV * 8;
+  static constexpr size_t SMEM_XF = size_t(ROWS) * XSF * 8;
+  static constexpr size_t SMEM_OP = size_t(Shape<N>::OPN) * 8;
+  static constexpr size_t SMEM_IN = size_t(2) * BIN;
+  static constexpr size_t SMEM_PR = size_t(3) * EB * Shape<N>::NP * 8;   // own-node 1/rho, p, c
   static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_IN + SMEM_T + 16;
+  static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_PR + SMEM_T + 16;
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
-  static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5, BAR_Q_EMPTY = 6;
+  static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
+                       BAR_Q_EMPTY = 6 /* and 7 */, BAR_C = 8;
 };
+
+template <int N, int MODE>
+struct ConsumerIO {
+  const StageArgs& A;
+  double* sXv;
+  double* sXf;
+  const double* sOp;
+  unsigned char* in0;
+  int nmine, ctid, lane;
+};
+
+template <int N, int MODE, int NPAIR, int NSING>
+__device__ __forceinline__ void ws_consumer(const ConsumerIO<N, MODE>& io, int cw, int s0) {
+  using S = Shape<N>;
+  using W = WS<N>;
+  constexpr int NP = S::NP, EB = W::EB, NT = W::NT, XSV = W::XSV, XSF = W::XSF;
+  constexpr int NPG = S::NTL / 2;
+  const StageArgs& A = io.A;
+  const int lane = io.lane, g = lane >> 2, t4 = lane & 3;
+  // this warp's units
+  int mtp[NPAIR > 0 ? NPAIR : 1], ntp[NPAIR > 0 ? NPAIR : 1], mts[NSING > 0 ? NSING : 1];
+#pragma unroll
+  for (int k = 0; k < NPAIR; ++k) {
+    const int p = cw + k * W::CW;
+    mtp[k] = p / NPG;
+    ntp[k] = 2 * (p % NPG);
+  }
+#pragma unroll
+  for (int k = 0; k < NSING; ++k) mts[k] = s0 + k * W::CW;
+  constexpr int NSLOT = 2 * NPAIR + NSING;   // n-tiles handled per k-step
+  for (int j = 0; j < io.nmine; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    const int e0 = A.e_begin + tile * EB;
+    const int ne = min(EB, A.e_end - e0);
+    const int buf = j & 1;
+    double* q_s = reinterpret_cast<double*>(io.in0 + buf * W::BIN);
+    double acc[NSLOT > 0 ? NSLOT : 1][4];
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+    auto kloop = [&](auto xblk) {
+      constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
+      if (A.debug & 1) return;
+      const double* X = (K0 == 0) ? io.sXv : io.sXf;
+#pragma unroll 4
+      for (int ks = K0; ks < K1; ++ks) {
+        const double* ob = io.sOp + ks * S::NTL * 32;
+#pragma unroll
+        for (int k = 0; k < NPAIR; ++k) {
+          const double* xa = X + (mtp[k] * 16 + g) * XSTR + t4 + (ks - K0) * 4;
+          const double a0 = xa[0], a1 = xa[8 * XSTR];
+          const double2 b = *reinterpret_cast<const double2*>(ob + ntp[k] * 32 + 2 * lane);
+          dmma_16x8x4(acc[2 * k], a0, a1, b.x);
+          dmma_16x8x4(acc[2 * k + 1], a0, a1, b.y);
+        }
+#pragma unroll
+        for (int k = 0; k < NSING; ++k) {
+          const double* xa = X + (mts[k] * 16 + g) * XSTR + t4 + (ks - K0) * 4;
+          const double a0 = xa[0], a1 = xa[8 * XSTR];
+          dmma_16x8x4(acc[2 * NPAIR + k], a0, a1, ob[(S::NTL - 1) * 32 + lane]);
+        }
+      }
+    };
+    // unit u -> (m-tile, n-tile)
+    auto unit_mt = [&](int u) { return u < 2 * NPAIR ? mtp[u >> 1] : mts[u - 2 * NPAIR]; };
+    auto unit_nt = [&](int u) { return u < 2 * NPAIR ? ntp[u >> 1] + (u & 1) : S::NTL - 1; };
+    nbar_sync(W::BAR_XV_FULL, NT);
+    kloop(KBlk<XSV, 0, S::KSV>{});
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+    // prefetch the residual while the face block of X is produced
+    double rprev[NSLOT > 0 ? NSLOT : 1][4];
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int row = unit_mt(u) * 16 + g + 8 * h, e = row / 5;
+          const int n = unit_nt(u) * 8 + 2 * t4 + q;
+          const bool ok = MODE == MODE_UPDATE && e < ne && n < NP;
+          rprev[u][2 * h + q] = ok ? __ldg(A.res + size_t(e0) * 5 * NP + row * NP + n) : 0.0;
+        }
+    nbar_sync(W::BAR_XF_FULL, NT);
+    kloop(KBlk<XSF, S::KSV, S::KS4>{});
+    // epilogue: full tiles stage res (in the face block of X) and Q (in place) for TMA bulk stores
+    const bool staged = MODE == MODE_UPDATE && ne == EB;
+    if (staged) nbar_sync(W::BAR_C, W::CT);       // every consumer is done reading Xf
+    double* sRes = io.sXf;
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = unit_mt(u) * 16 + g + 8 * h;
+        const int e = row / 5, c = row - 5 * (row / 5);
+        if (e >= ne) continue;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = unit_nt(u) * 8 + 2 * t4 + q;
+          if (n >= NP) continue;
+          const double rhs = acc[u][2 * h + q];
+          const int li = row * NP + n;           // == (e*5 + c)*NP + n
+          if (MODE == MODE_UPDATE) {
+            const double rr = fma(A.a, rprev[u][2 * h + q], A.dt * rhs);
+            const double qn = fma(A.b, rr, q_s[li]);
+            if (staged) {
+              sRes[li] = rr;
+              q_s[li] = qn;
+            } else {
+              const size_t gi = size_t(e0) * 5 * NP + li;
+              A.res[gi] = rr;
+              A.Qout[gi] = qn;
+            }
+          } else {
+            A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
+          }
+        }
+      }
+    }
+    if (staged) {
+      nbar_sync(W::BAR_C, W::CT);
+      if (io.ctid == 0) {
+        fence_proxy_async();
+        tma_store_1d(A.res + size_t(e0) * 5 * NP, sRes, W::BQ);
+        tma_store_1d(A.Qout + size_t(e0) * 5 * NP, q_s, W::BQ);
+        tma_store_commit_and_wait_read();
+      }
+      nbar_sync(W::BAR_C, W::CT);
+    }
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
+    if (j + 2 < io.nmine) nbar_arrive(W::BAR_Q_EMPTY + buf, NT);
+  }
+  // make the last bulk stores globally visible before the kernel ends
+  if (io.ctid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
 
 template <int N, int MODE>
 __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs A) {
   using S = Shape<N>;
   using W = WS<N>;
-  constexpr int NP = S::NP, NFP = S::NFP, EB = W::EB, XS = S::XS, NT = W::NT;
-  constexpr int PT = 32 * W::PW;
+  constexpr int NP = S::NP, NFP = S::NFP, EB = W::EB, NT = W::NT, PT = W::PT;
+  constexpr int XSV = W::XSV, XSF = W::XSF;
   extern __shared__ __align__(128) unsigned char smem[];
-  double* sX = reinterpret_cast<double*>(smem);
-  double* sOp = sX + W::ROWS * XS;
-  unsigned char* in0 = reinterpret_cast<unsigned char*>(sOp + W::OPS);
-  // per buffer b: Q | geo | nbr | code
-  auto bufQ = [&](int b) { return reinterpret_cast<double*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC)); };
-  auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ); };
-  auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ + W::BG); };
-  auto bufC = [&](int b) {
-    return reinterpret_cast<uint8_t*>(in0 + b * (W::BQ + W::BG + W::BN + W::BC) + W::BQ + W::BG + W::BN);
-  };
-  uint8_t* sTbl = in0 + 2 * (W::BQ + W::BG + W::BN + W::BC);
+  double* sXv = reinterpret_cast<double*>(smem);
+  double* sXf = sXv + W::ROWS * XSV;
+  double* sOp = sXf + W::ROWS * XSF;
+  unsigned char* in0 = reinterpret_cast<unsigned char*>(sOp + S::OPN);
+  auto bufQ = [&](int b) { return reinterpret_cast<double*>(in0 + b * W::BIN); };
+  auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * W::BIN + W::BQ); };
+  auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * W::BIN + W::BQ + W::BG); };
+  auto bufC = [&](int b) { return reinterpret_cast<uint8_t*>(in0 + b * W::BIN + W::BQ + W::BG + W::BN); };
+  double* sRi = reinterpret_cast<double*>(in0 + 2 * W::BIN);   // own-node 1/rho, p, c of the current tile
+  double* sPr = sRi + EB * NP;
+  double* sCs = sPr + EB * NP;
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sCs + EB * NP);
   uint8_t* sTblf = sTbl + 96 * NFP;
   uint8_t* sFm = sTblf + 96 * NFP;
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // B operand regrouped per (k-step, n-tile group): lane reads its NTG values contiguously
-  for (int i = tid; i < W::OPS; i += NT) {
-    const int l = i % (32 * W::NTG), rest = i / (32 * W::NTG);
-    const int grp = rest % W::NGRP, ks = rest / W::NGRP;
-    const int ln = l / W::NTG, jj = l % W::NTG, nt = grp * W::NTG + jj;
-    sOp[i] = nt < S::NTL ? A.op[(ks * S::NTL + nt) * 32 + ln] : 0.0;
+  // B operand regrouped per (k-step, n-tile group): a lane reads its group's values contiguously
+  for (int i = tid; i < S::OPN; i += NT) {
+    const int ks = i / (S::NTL * 32), r = i - ks * S::NTL * 32;
+    const int grp = r / (W::NTG * 32), rr = r - grp * W::NTG * 32;
+    const int gsz = min(W::NTG, S::NTL - grp * W::NTG);
+    const int ln = rr / gsz, jj = rr - ln * gsz, nt = grp * W::NTG + jj;
+    sOp[i] = A.op[(ks * S::NTL + nt) * 32 + ln];
   }
   for (int i = tid; i < 96 * NFP; i += NT) {
     sTbl[i] = A.tbl[i];
     sTblf[i] = A.tblf[i];
   }
   for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
-  for (int i = tid; i < W::ROWS * XS; i += NT) sX[i] = 0.0;   // padding columns stay 0
+  for (int i = tid; i < W::ROWS * (XSV + XSF); i += NT) sXv[i] = 0.0;   // padding columns stay 0
   if (tid == 0) {
     mbar_init(&sBar[0], 1);
     mbar_init(&sBar[1], 1);
@@ -439,13 +615,11 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   __syncthreads();
 
   const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
-  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (warp < W::PW) {
     // ======================= producers: load (TMA), volume flux, face flux
     const double gamma = A.gamma, gm1 = A.gamma - 1.0;
-    // inputs of local tile jj into buffer jj&1: TMA bulk copies for a full tile, plain loads otherwise
     auto fetch = [&](int jj) {
       const int tile = blockIdx.x + jj * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
@@ -454,7 +628,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ne == EB) {
         if (tid == 0) {
           fence_proxy_async();
-          mbar_arrive_expect_tx(&sBar[b], W::BQ + W::BG + W::BN + W::BC);
+          mbar_arrive_expect_tx(&sBar[b], W::BIN);
           tma_load_1d(bufQ(b), A.Qin + size_t(e0) * 5 * NP, W::BQ, &sBar[b]);
           tma_load_1d(bufG(b), A.geo + size_t(e0) * GEO, W::BG, &sBar[b]);
           tma_load_1d(bufN(b), A.nbr + size_t(e0) * 4, W::BN, &sBar[b]);
@@ -485,44 +659,69 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int* n_s = bufN(buf);
       const uint8_t* c_s = bufC(buf);
       if (ne == EB) mbar_wait(&sBar[buf], (j >> 1) & 1);
-      // ---- volume fluxes -> X[:, 0:3NP)
+      // ---- volume fluxes -> Xv; own-node 1/rho, p, c -> sRi/sPr/sCs for the face phase
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
-      for (int idx = tid; idx < EB * NP; idx += PT) {
+      for (int idx = tid; idx < ((A.debug & 2) ? 0 : EB * NP); idx += PT) {
         const int e = idx / NP, n = idx - e * NP;
-        double* xr = sX + (e * 5) * XS + n;
+        double* xr = sXv + (e * 5) * XSV + n;
         if (e < ne) {
-          volume_node<NP, XS>(q_s + e * 5 * NP + n, g_s + e * GEO, xr, gm1, A.pref, A.flag, A.gid[e0 + e]);
+          const double* q = q_s + e * 5 * NP + n;
+          const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
+          const double ri = rcp_nr(rho);
+          const double u = mx * ri, v = my * ri, w = mz * ri;
+          const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
+          if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(A.flag, A.gid[e0 + e]);
+          sRi[idx] = ri;
+          sPr[idx] = p;
+          sCs[idx] = sqrt_nr(gamma * p * ri);
+          const double* G = g_s + e * GEO;
+          const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
+            const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
+            double* xc = xr + d * NP;
+            xc[0] = rho * U;
+            xc[XSV] = fma(cx, pd, mx * U);
+            xc[2 * XSV] = fma(cy, pd, my * U);
+            xc[3 * XSV] = fma(cz, pd, mz * U);
+            xc[4 * XSV] = Ep * U;
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
-            xr[c * XS] = 0.0;
-            xr[c * XS + NP] = 0.0;
-            xr[c * XS + 2 * NP] = 0.0;
+            xr[c * XSV] = 0.0;
+            xr[c * XSV + NP] = 0.0;
+            xr[c * XSV + 2 * NP] = 0.0;
           }
         }
       }
       nbar_arrive(W::BAR_XV_FULL, NT);
+      nbar_sync(W::BAR_P, PT);                      // sRi/sPr/sCs complete for the face phase
       // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1)
       if (j + 1 < nmine) {
         if (j + 1 >= 2) nbar_sync(W::BAR_Q_EMPTY + ((j + 1) & 1), NT);
         fetch(j + 1);
       }
-      // ---- face fluxes -> X[:, KVP:KVP+4NFP): one face per NFP-lane segment, two passes at a time
+      // ---- face fluxes -> Xf: one face per NFP-lane segment, two passes at a time
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
       const int seg = lane / NFP, i = lane - seg * NFP;
       const bool lane_ok = seg < W::NSEG;
       constexpr int STRIDE = W::PW * W::NSEG;
-      for (int fb = warp * W::NSEG; fb < EB * 4; fb += 2 * STRIDE) {
+      for (int fb = warp * W::NSEG; fb < ((A.debug & 2) ? 0 : EB * 4); fb += 2 * STRIDE) {
         double qm[2][5], qp[2][5], nv[2][4];
+        int vm[2];
         bool act[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int face = fb + u * STRIDE + seg;
           const int e = face >> 2, f = face & 3;
           act[u] = lane_ok && face < EB * 4 && e < ne;
+          vm[u] = 0;
           if (act[u]) {
             const double* G = g_s + e * GEO + 9 + 4 * f;
             nv[u][0] = G[0]; nv[u][1] = G[1]; nv[u][2] = G[2]; nv[u][3] = G[3];
+            vm[u] = e * NP + sFm[f * NFP + i];
             const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
 #pragma unroll
             for (int c = 0; c < 5; ++c) qm[u][c] = q[c * NP];
@@ -532,36 +731,41 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
+          if (fb + u * STRIDE >= EB * 4) break;   // warp-uniform
           const int face = fb + u * STRIDE + seg;
           const int e = face >> 2, f = face & 3;
-          if (fb + u * STRIDE >= EB * 4) break;   // warp-uniform
-          double lam = 0.0;
-          SideFlux sm, sp;
+          double lam = 0.0, dq[5], df[5];
           if (act[u]) {
-            sm = side_flux(qm[u], nv[u][0], nv[u][1], nv[u][2], gamma, A.pref);
-            sp = side_flux(qp[u], nv[u][0], nv[u][1], nv[u][2], gamma, A.pref);
-            lam = fmax(sm.speed, sp.speed);
+            const double nx = nv[u][0], ny = nv[u][1], nz = nv[u][2];
+            // own side from the volume phase's primitives
+            const double rim = sRi[vm[u]], pm = sPr[vm[u]];
+            const double unm = (qm[u][1] * nx + qm[u][2] * ny + qm[u][3] * nz) * rim;
+            const double pdm = pm - A.pref;
+            const SideFlux sp = side_flux(qp[u], nx, ny, nz, gamma, A.pref);
+            df[0] = qm[u][0] * unm - sp.f[0];
+            df[1] = fma(pdm, nx, qm[u][1] * unm) - sp.f[1];
+            df[2] = fma(pdm, ny, qm[u][2] * unm) - sp.f[2];
+            df[3] = fma(pdm, nz, qm[u][3] * unm) - sp.f[3];
+            df[4] = (qm[u][4] + pm) * unm - sp.f[4];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) dq[c] = qp[u][c] - qm[u][c];
+            lam = fmax(fabs(unm) + sCs[vm[u]], sp.speed);
           }
           if (A.lambda_mode == 0) {
             // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+            for (int d = 1; d < NFP; d <<= 1) {
               const double o = __shfl_up_sync(0xffffffffu, lam, d);
               if (lane_ok && i >= d) lam = fmax(lam, o);
             }
             lam = __shfl_sync(0xffffffffu, lam, lane_ok ? seg * NFP + NFP - 1 : lane);
           }
-          if (act[u]) {
-            double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+          if (lane_ok && face < EB * 4) {
+            // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
+            double* xd = sXf + (e * 5) * XSF + f * NFP + i;
+            const double hfs = 0.5 * nv[u][3];
 #pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[u][c] - qm[u][c]);
-              xd[c * XS] = nv[u][3] * (sm.f[c] - fstar);
-            }
-          } else if (lane_ok && face < EB * 4) {
-            double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) xd[c * XS] = 0.0;
+            for (int c = 0; c < 5; ++c) xd[c * XSF] = act[u] ? hfs * fma(lam, dq[c], df[c]) : 0.0;
           }
         }
       }
@@ -569,98 +773,20 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     }
   } else {
     // ======================= consumers: DMMA contraction + LSERK epilogue
-    const int cw = warp - W::PW, g = lane >> 2, t4 = lane & 3;
-    int mt[W::IPW], ng[W::IPW];
-    bool on[W::IPW];
-#pragma unroll
-    for (int it = 0; it < W::IPW; ++it) {
-      const int item = cw + it * W::CW;
-      on[it] = item < W::ITEMS;
-      mt[it] = on[it] ? item / W::NGRP : 0;
-      ng[it] = on[it] ? item - mt[it] * W::NGRP : 0;
-    }
-    for (int j = 0; j < nmine; ++j) {
-      const int tile = blockIdx.x + j * gridDim.x;
-      const int e0 = A.e_begin + tile * EB;
-      const int ne = min(EB, A.e_end - e0);
-      const int buf = j & 1;
-      const double* q_s = bufQ(buf);
-      double acc[W::IPW][W::NTG][4];
-#pragma unroll
-      for (int it = 0; it < W::IPW; ++it)
-#pragma unroll
-        for (int jj = 0; jj < W::NTG; ++jj) acc[it][jj][0] = acc[it][jj][1] = acc[it][jj][2] = acc[it][jj][3] = 0.0;
-      auto kloop = [&](int k0, int k1) {
-#pragma unroll 4
-        for (int ks = k0; ks < k1; ++ks) {
-#pragma unroll
-          for (int it = 0; it < W::IPW; ++it) {
-            if (!on[it]) continue;
-            const double* xa = sX + (mt[it] * 16 + g) * XS + t4 + ks * 4;
-            const double a0 = xa[0], a1 = xa[8 * XS];
-            const double* ob = sOp + ((ks * W::NGRP + ng[it]) * 32 + lane) * W::NTG;
-            if constexpr (W::NTG == 2) {
-              const double2 b = *reinterpret_cast<const double2*>(ob);
-              dmma_16x8x4(acc[it][0], a0, a1, b.x);
-              dmma_16x8x4(acc[it][1], a0, a1, b.y);
-            } else {
-              dmma_16x8x4(acc[it][0], a0, a1, ob[0]);
-            }
-          }
-        }
-      };
-      nbar_sync(W::BAR_XV_FULL, NT);
-      kloop(0, S::KSV);
-      if (j + 1 < nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
-      // prefetch the residual while the face half of X is produced
-      double rprev[W::IPW][W::NTG][4];
-#pragma unroll
-      for (int it = 0; it < W::IPW; ++it)
-#pragma unroll
-        for (int jj = 0; jj < W::NTG; ++jj)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int row = mt[it] * 16 + g + 8 * h, e = row / 5, c = row - 5 * (row / 5);
-              const int n = (ng[it] * W::NTG + jj) * 8 + 2 * t4 + q;
-              const bool ok = MODE == MODE_UPDATE && on[it] && e < ne && n < NP;
-              rprev[it][jj][2 * h + q] = ok ? __ldg(A.res + (size_t(e0 + e) * 5 + c) * NP + n) : 0.0;
-            }
-      nbar_sync(W::BAR_XF_FULL, NT);
-      kloop(S::KSV, S::KS4);
-      if (j + 1 < nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
-#pragma unroll
-      for (int it = 0; it < W::IPW; ++it) {
-        if (!on[it]) continue;
-#pragma unroll
-        for (int jj = 0; jj < W::NTG; ++jj) {
-          const int nt = ng[it] * W::NTG + jj;
-          if (nt >= S::NTL) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int row = mt[it] * 16 + g + 8 * h;
-            const int e = row / 5, c = row - 5 * (row / 5);
-            if (e >= ne) continue;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int n = nt * 8 + 2 * t4 + q;
-              if (n >= NP) continue;
-              const double rhs = acc[it][jj][2 * h + q];
-              if (MODE == MODE_UPDATE) {
-                const size_t gi = (size_t(e0 + e) * 5 + c) * NP + n;
-                const double rr = fma(A.a, rprev[it][jj][2 * h + q], A.dt * rhs);
-                A.res[gi] = rr;
-                A.Qout[gi] = fma(A.b, rr, q_s[(e * 5 + c) * NP + n]);
-              } else {
-                A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
-              }
-            }
-          }
-        }
-      }
-      if (j + 2 < nmine) nbar_arrive(W::BAR_Q_EMPTY + buf, NT);
-    }
+    // Work units are (m-tile, n-tile pair) and (m-tile, trailing odd n-tile); every warp runs a
+    // compile-time-shaped loop so its DMMA chains interleave without run-time branches.
+    constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
+    constexpr int P = W::MT * NPG, SG = W::MT * HS;
+    constexpr int CPMAX = (P + W::CW - 1) / W::CW, CSMAX = (SG + W::CW - 1) / W::CW;
+    const int cw = warp - W::PW;
+    const int cp = P > cw ? (P - 1 - cw) / W::CW + 1 : 0;
+    const int s0 = ((cw - P % W::CW) % W::CW + W::CW) % W::CW;     // first single of this warp
+    const int cs = SG > s0 ? (SG - 1 - s0) / W::CW + 1 : 0;
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, nmine, tid - W::PT, lane};
+    if (cp == CPMAX && cs == CSMAX) ws_consumer<N, MODE, CPMAX, CSMAX>(io, cw, s0);
+    else if (cp == CPMAX && cs == CSMAX - 1) ws_consumer<N, MODE, CPMAX, (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
+    else if (cp == CPMAX - 1 && cs == CSMAX) ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), CSMAX>(io, cw, s0);
+    else ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
   }
 }
 
