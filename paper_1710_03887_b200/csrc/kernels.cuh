@@ -180,6 +180,39 @@ __device__ __forceinline__ void exterior_trace(const StageArgs& A, int code, int
   }
 }
 
+// Neighbour trace for a paired face (local element or halo record); boundary faces are filled later.
+template <int NP, int NFP>
+__device__ __forceinline__ void gather_trace(const StageArgs& A, int code, int nb, int f, int i, const uint8_t* tbl,
+                                             const uint8_t* tblf, double (&qp)[5]) {
+  if (code < CODE_GHOST) {
+    const double* q2 = A.Qin + size_t(nb) * 5 * NP + tbl[(f * 24 + code) * NFP + i];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NP);
+  } else if (code < CODE_BC) {
+    const double* q2 = A.recv + size_t(nb) * 5 * NFP + tblf[(f * 24 + code - CODE_GHOST) * NFP + i];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NFP);
+  }
+}
+
+// Boundary ghost of face node with interior trace qm (wall: Eq. 4 mirror, pass-through: Eq. 3, inflow: Eqs. 5-7).
+__device__ __forceinline__ void ghost_trace(const StageArgs& A, int tag, const double (&qm)[5], double nx, double ny,
+                                            double nz, double (&qp)[5]) {
+  if (tag == 1) {
+    const double mn = qm[1] * nx + qm[2] * ny + qm[3] * nz;
+    qp[0] = qm[0];
+    qp[1] = qm[1] - 2.0 * mn * nx;
+    qp[2] = qm[2] - 2.0 * mn * ny;
+    qp[3] = qm[3] - 2.0 * mn * nz;
+    qp[4] = qm[4];
+  } else if (tag == 2) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[c] = A.qinf[c];
+  } else {
+    inflow_state(A.t, A.inflow_alpha, A.gamma, qp);
+  }
+}
+
 struct SideFlux {
   double f[5];   // n.F(q) with the ambient pressure subtracted (A14)
   double speed;  // |u.n| + c
@@ -403,7 +436,14 @@ struct KBlk {
 template <int N>
 struct WS {
   static constexpr int EB = (N <= 2) ? 32 : 16;
-  static constexpr int PW = 8, CW = 8;                      // producer / consumer warps
+#ifndef DG_WS_PW
+#define DG_WS_PW 8
+#endif
+#ifndef DG_FACE_BATCH
+#define DG_FACE_BATCH 2
+#endif
+  static constexpr int PW = DG_WS_PW, CW = 8;               // producer / consumer warps
+  static constexpr int FB = DG_FACE_BATCH;                  // face passes batched per producer iteration
   static constexpr int NT = 32 * (PW + CW);
   static constexpr int PT = 32 * PW, CT = 32 * CW;
   static constexpr int ROWS = 5 * EB;                       // multiple of 16
@@ -501,10 +541,7 @@ __device__ __forceinline__ void ws_consumer(const ConsumerIO<N, MODE>& io, int c
     // unit u -> (m-tile, n-tile)
     auto unit_mt = [&](int u) { return u < 2 * NPAIR ? mtp[u >> 1] : mts[u - 2 * NPAIR]; };
     auto unit_nt = [&](int u) { return u < 2 * NPAIR ? ntp[u >> 1] + (u & 1) : S::NTL - 1; };
-    nbar_sync(W::BAR_XV_FULL, NT);
-    kloop(KBlk<XSV, 0, S::KSV>{});
-    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
-    // prefetch the residual while the face block of X is produced
+    // prefetch the residual for the epilogue: issued before the GEMM so HBM latency hides behind it
     double rprev[NSLOT > 0 ? NSLOT : 1][4];
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u)
@@ -517,6 +554,9 @@ __device__ __forceinline__ void ws_consumer(const ConsumerIO<N, MODE>& io, int c
           const bool ok = MODE == MODE_UPDATE && e < ne && n < NP;
           rprev[u][2 * h + q] = ok ? __ldg(A.res + size_t(e0) * 5 * NP + row * NP + n) : 0.0;
         }
+    nbar_sync(W::BAR_XV_FULL, NT);
+    kloop(KBlk<XSV, 0, S::KSV>{});
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
     nbar_sync(W::BAR_XF_FULL, NT);
     kloop(KBlk<XSF, S::KSV, S::KS4>{});
     // epilogue: full tiles stage res (in the face block of X) and Q (in place) for TMA bulk stores
@@ -659,6 +699,22 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int* n_s = bufN(buf);
       const uint8_t* c_s = bufC(buf);
       if (ne == EB) mbar_wait(&sBar[buf], (j >> 1) & 1);
+      // ---- issue this warp's neighbour-trace gathers for the whole tile first: their latency
+      //      hides behind the volume phase (one face per NFP-lane segment, FPASS passes)
+      const int seg = lane / NFP, i = lane - seg * NFP;
+      const bool lane_ok = seg < W::NSEG;
+      constexpr int STRIDE = W::PW * W::NSEG;
+      constexpr int FPASS = (EB * 4 + STRIDE - 1) / STRIDE;
+      double qp[FPASS][5];
+#pragma unroll
+      for (int u = 0; u < FPASS; ++u) {
+        const int face = warp * W::NSEG + u * STRIDE + seg;
+        const int e = face >> 2, f = face & 3;
+        if (!(A.debug & 2) && lane_ok && face < EB * 4 && e < ne) {
+          const int code = c_s[e * 4 + f];
+          if (code < CODE_BC) gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
+        }
+      }
       // ---- volume fluxes -> Xv; own-node 1/rho, p, c -> sRi/sPr/sCs for the face phase
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       for (int idx = tid; idx < ((A.debug & 2) ? 0 : EB * NP); idx += PT) {
@@ -703,70 +759,55 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         if (j + 1 >= 2) nbar_sync(W::BAR_Q_EMPTY + ((j + 1) & 1), NT);
         fetch(j + 1);
       }
-      // ---- face fluxes -> Xf: one face per NFP-lane segment, two passes at a time
+      // ---- face fluxes -> Xf
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
-      const int seg = lane / NFP, i = lane - seg * NFP;
-      const bool lane_ok = seg < W::NSEG;
-      constexpr int STRIDE = W::PW * W::NSEG;
-      for (int fb = warp * W::NSEG; fb < ((A.debug & 2) ? 0 : EB * 4); fb += 2 * STRIDE) {
-        double qm[2][5], qp[2][5], nv[2][4];
-        int vm[2];
-        bool act[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int face = fb + u * STRIDE + seg;
-          const int e = face >> 2, f = face & 3;
-          act[u] = lane_ok && face < EB * 4 && e < ne;
-          vm[u] = 0;
-          if (act[u]) {
-            const double* G = g_s + e * GEO + 9 + 4 * f;
-            nv[u][0] = G[0]; nv[u][1] = G[1]; nv[u][2] = G[2]; nv[u][3] = G[3];
-            vm[u] = e * NP + sFm[f * NFP + i];
-            const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+      for (int u = 0; u < FPASS; ++u) {
+        if (warp * W::NSEG + u * STRIDE >= EB * 4) break;   // warp-uniform
+        if (A.debug & 2) break;
+        const int face = warp * W::NSEG + u * STRIDE + seg;
+        const int e = face >> 2, f = face & 3;
+        const bool act = lane_ok && face < EB * 4 && e < ne;
+        double lam = 0.0, dq[5], df[5], hfs = 0.0;
+        if (act) {
+          const double* G = g_s + e * GEO + 9 + 4 * f;
+          const double nx = G[0], ny = G[1], nz = G[2];
+          hfs = 0.5 * G[3];
+          const int vm = e * NP + sFm[f * NFP + i];
+          const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+          double qm[5];
 #pragma unroll
-            for (int c = 0; c < 5; ++c) qm[u][c] = q[c * NP];
-            exterior_trace<NP, NFP>(A, c_s[e * 4 + f], n_s[e * 4 + f], f, i, sTbl, sTblf, qm[u], nv[u][0], nv[u][1],
-                                    nv[u][2], qp[u]);
-          }
+          for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+          const int code = c_s[e * 4 + f];
+          if (code >= CODE_BC) ghost_trace(A, code - CODE_BC, qm, nx, ny, nz, qp[u]);
+          // own side from the volume phase's primitives
+          const double rim = sRi[vm], pm = sPr[vm];
+          const double unm = (qm[1] * nx + qm[2] * ny + qm[3] * nz) * rim;
+          const double pdm = pm - A.pref;
+          const SideFlux sp = side_flux(qp[u], nx, ny, nz, gamma, A.pref);
+          df[0] = qm[0] * unm - sp.f[0];
+          df[1] = fma(pdm, nx, qm[1] * unm) - sp.f[1];
+          df[2] = fma(pdm, ny, qm[2] * unm) - sp.f[2];
+          df[3] = fma(pdm, nz, qm[3] * unm) - sp.f[3];
+          df[4] = (qm[4] + pm) * unm - sp.f[4];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) dq[c] = qp[u][c] - qm[c];
+          lam = fmax(fabs(unm) + sCs[vm], sp.speed);
         }
+        if (A.lambda_mode == 0) {
+          // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (fb + u * STRIDE >= EB * 4) break;   // warp-uniform
-          const int face = fb + u * STRIDE + seg;
-          const int e = face >> 2, f = face & 3;
-          double lam = 0.0, dq[5], df[5];
-          if (act[u]) {
-            const double nx = nv[u][0], ny = nv[u][1], nz = nv[u][2];
-            // own side from the volume phase's primitives
-            const double rim = sRi[vm[u]], pm = sPr[vm[u]];
-            const double unm = (qm[u][1] * nx + qm[u][2] * ny + qm[u][3] * nz) * rim;
-            const double pdm = pm - A.pref;
-            const SideFlux sp = side_flux(qp[u], nx, ny, nz, gamma, A.pref);
-            df[0] = qm[u][0] * unm - sp.f[0];
-            df[1] = fma(pdm, nx, qm[u][1] * unm) - sp.f[1];
-            df[2] = fma(pdm, ny, qm[u][2] * unm) - sp.f[2];
-            df[3] = fma(pdm, nz, qm[u][3] * unm) - sp.f[3];
-            df[4] = (qm[u][4] + pm) * unm - sp.f[4];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) dq[c] = qp[u][c] - qm[u][c];
-            lam = fmax(fabs(unm) + sCs[vm[u]], sp.speed);
+          for (int d = 1; d < NFP; d <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, lam, d);
+            if (lane_ok && i >= d) lam = fmax(lam, o);
           }
-          if (A.lambda_mode == 0) {
-            // segmented max over the face's NFP lanes: inclusive scan, then broadcast the last
+          lam = __shfl_sync(0xffffffffu, lam, lane_ok ? seg * NFP + NFP - 1 : lane);
+        }
+        if (lane_ok && face < EB * 4) {
+          // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
+          double* xd = sXf + (e * 5) * XSF + f * NFP + i;
 #pragma unroll
-            for (int d = 1; d < NFP; d <<= 1) {
-              const double o = __shfl_up_sync(0xffffffffu, lam, d);
-              if (lane_ok && i >= d) lam = fmax(lam, o);
-            }
-            lam = __shfl_sync(0xffffffffu, lam, lane_ok ? seg * NFP + NFP - 1 : lane);
-          }
-          if (lane_ok && face < EB * 4) {
-            // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
-            double* xd = sXf + (e * 5) * XSF + f * NFP + i;
-            const double hfs = 0.5 * nv[u][3];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) xd[c * XSF] = act[u] ? hfs * fma(lam, dq[c], df[c]) : 0.0;
-          }
+          for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam, dq[c], df[c]) : 0.0;
         }
       }
       nbar_arrive(W::BAR_XF_FULL, NT);
