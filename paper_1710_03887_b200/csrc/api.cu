@@ -156,6 +156,7 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   A.inflow_alpha = c->inflow_alpha;
   A.lambda_mode = c->lambda_mode;
   if (const char* dbg = std::getenv("DG_DEBUG_TIMING")) A.debug = std::atoi(dbg);
+  A.trace = reinterpret_cast<unsigned long long*>(c->dscratch);
   const double* qi = c->q_inf;
   A.pref = (c->gamma - 1.0) * (qi[4] - 0.5 * (qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]) / qi[0]);
   return A;
@@ -622,5 +623,12 @@ dg_status dg_get_geometry(const dg_ctx* c, double* J, double* rx9, double* n12, 
 }
 
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+// Debug only (DG_TRACE builds): copy the phase-timestamp scratch of the last stage launch.
+dg_status dg_debug_trace(const dg_ctx* c, unsigned long long* out, int n) {
+  if (!c || !c->ws || !out || n <= 0 || n > 4096) return set_err(nullptr, DG_EARG, "bad argument");
+  CUDA_TRY(nullptr, cudaMemcpy(out, c->dscratch, size_t(n) * 8, cudaMemcpyDeviceToHost));
+  return DG_OK;
+}
 
 }  // extern "C"

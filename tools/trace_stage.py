@@ -1,0 +1,33 @@
+"""Phase timeline of one CTA of the C4 stage kernel (needs a DG_TRACE=1 build)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1710_03887_b200 as dg  # noqa: E402
+from synth import configs  # noqa: E402
+
+cfg = configs.make(sys.argv[1] if len(sys.argv) > 1 else "C4")
+m = cfg.mesh
+s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma, q_inf=cfg.q_inf)
+s.set_state(configs.initial_state(cfg, s.nodes()))
+dt = s.stable_dt(0.5)
+s.step(dt, 2)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 1024)()
+f = dg._lib.dg_debug_trace
+f.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_int]
+f.restype = C.c_int
+assert f(s.ctx, buf, 1024) == 0
+t = np.array(buf, dtype=np.int64).reshape(64, 16)
+names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi",
+         8: "P start", 9: "P tma", 10: "P XVempty", 11: "P vol", 12: "P fetch", 13: "P XFempty", 14: "P face"}
+t0 = t[2, 0]
+for j in range(2, 8):
+    row = t[j]
+    print(f"tile {j}: " + "  ".join(f"{names[e]}={row[e] - t0}" for e in sorted(names)))
+per = (t[10, 0] - t[2, 0]) / 8
+print("cycles per tile (tiles 2..10):", per)
