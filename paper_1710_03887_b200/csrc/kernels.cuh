@@ -484,13 +484,17 @@ struct WS {
   static constexpr size_t SMEM_IN = size_t(2) * BIN;
   static constexpr size_t SMEM_PR = size_t(3) * EB * Shape<N>::NP * 8;   // own-node 1/rho, p, c
   static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM_L = size_t(PW) * 32 * 8;                  // per-warp face-speed exchange
-  static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_PR + SMEM_L + SMEM_T + 16;
+  static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_PR + SMEM_T + 16;
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
   static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
                        BAR_Q_EMPTY = 6 /* and 7 */, BAR_C = 8;
 };
+
+#ifndef DG_KUNROLL
+#define DG_KUNROLL 4
+#endif
+constexpr int KUNROLL = DG_KUNROLL;   // consumer k-loop unroll (register pressure vs load hoisting)
 
 template <int N, int MODE>
 struct ConsumerIO {
@@ -534,7 +538,7 @@ __device__ __forceinline__ void ws_consumer(const ConsumerIO<N, MODE>& io, int c
       constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
       if (A.debug & 1) return;
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
-#pragma unroll 4
+#pragma unroll KUNROLL
       for (int ks = K0; ks < K1; ++ks) {
         const double* ob = io.sOp + ks * S::NTL * 32;
 #pragma unroll
@@ -646,8 +650,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   double* sRi = reinterpret_cast<double*>(in0 + 2 * W::BIN);   // own-node 1/rho, p, c of the current tile
   double* sPr = sRi + EB * NP;
   double* sCs = sPr + EB * NP;
-  double* sLam = sCs + EB * NP;                                  // [PW][32]
-  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sLam + W::PW * 32);
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sCs + EB * NP);
   uint8_t* sTblf = sTbl + 96 * NFP;
   uint8_t* sFm = sTblf + 96 * NFP;
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);
