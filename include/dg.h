@@ -152,6 +152,11 @@ dg_status dg_halo_info(const dg_ctx* ctx, int* npeers, int64_t* nsend_total, int
 dg_status dg_halo_peer(const dg_ctx* ctx, int p, int* rank, int64_t* send_off, int64_t* nsend,
                        int64_t* recv_off, int64_t* nrecv);
 dg_status dg_halo_buffers(const dg_ctx* ctx, double** send, double** recv);
+/* Host description of the halo records (tests, custom transports): for send
+ * record s, the sender's global element id and local face; for receive record
+ * g, the remote (sender) global element id and face.  Arrays of nsend / nrecv. */
+dg_status dg_halo_records(const dg_ctx* ctx, int64_t* send_gid, int8_t* send_face, int64_t* recv_gid,
+                          int8_t* recv_face);
 /* Stage-level driver for custom transports: pack this rank's partition-face
  * traces of the current state into the send buffer; then, once the recv
  * buffer holds the peers' records, run stage s (0-based) of the RK scheme on

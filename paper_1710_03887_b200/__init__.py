@@ -27,7 +27,7 @@ SYMBOLS = (
     "dg_mesh_create", "dg_destroy", "dg_last_error", "dg_sizes", "dg_workspace_bytes", "dg_bind_workspace",
     "dg_memory_report", "dg_get_nodes", "dg_set_state", "dg_get_state", "dg_get_time", "dg_rhs", "dg_rk_step",
     "dg_check", "dg_stable_dt", "dg_nccl_get_unique_id", "dg_comm_init", "dg_halo_info", "dg_halo_peer",
-    "dg_halo_buffers", "dg_stage_pack", "dg_stage_compute", "dg_stage_finish", "dg_rhs_compute",
+    "dg_halo_buffers", "dg_halo_records", "dg_stage_pack", "dg_stage_compute", "dg_stage_finish", "dg_rhs_compute",
     "dg_get_operators", "dg_get_maps", "dg_get_geometry", "dg_launch_count",
 )
 
@@ -87,6 +87,7 @@ def _load():
         "dg_halo_info": (I, [P, C.POINTER(I), pi64, pi64]),
         "dg_halo_peer": (I, [P, I, C.POINTER(I), pi64, pi64, pi64, pi64]),
         "dg_halo_buffers": (I, [P, C.POINTER(P), C.POINTER(P)]),
+        "dg_halo_records": (I, [P, pi64, C.POINTER(C.c_int8), pi64, C.POINTER(C.c_int8)]),
         "dg_stage_pack": (I, [P, P]),
         "dg_stage_compute": (I, [P, I, D, I, P]),
         "dg_stage_finish": (I, [P, I, D]),
@@ -103,7 +104,24 @@ def _load():
     return lib
 
 
-_lib = _load()
+class _LazyLib:
+    """The shared library, loaded on first use (so `python -m paper_1710_03887_b200.build`
+    works on a fresh checkout); any use without the built library raises ImportError."""
+
+    _handle = None
+
+    def __getattr__(self, name):
+        if _LazyLib._handle is None:
+            _LazyLib._handle = _load()
+        return getattr(_LazyLib._handle, name)
+
+
+_lib = _LazyLib()
+
+
+def load():
+    """Load libdg_b200.so now (raises ImportError if it has not been built)."""
+    return _lib.dg_last_error
 
 
 def _ptr(a, ctype):
@@ -245,6 +263,15 @@ def dg_halo_buffers(ctx):
     s, r = C.c_void_p(), C.c_void_p()
     _check(_lib.dg_halo_buffers(ctx, C.byref(s), C.byref(r)), ctx)
     return s.value, r.value
+
+
+def dg_halo_records(ctx):
+    _, ns, nr = dg_halo_info(ctx)
+    sg, sf = np.empty(ns, dtype=np.int64), np.empty(ns, dtype=np.int8)
+    rg, rf = np.empty(nr, dtype=np.int64), np.empty(nr, dtype=np.int8)
+    _check(_lib.dg_halo_records(ctx, _ptr(sg, C.c_int64), _ptr(sf, C.c_int8), _ptr(rg, C.c_int64),
+                                _ptr(rf, C.c_int8)), ctx)
+    return sg, sf, rg, rf
 
 
 def dg_stage_pack(ctx, stream: int):

@@ -563,6 +563,19 @@ dg_status dg_halo_buffers(const dg_ctx* c, double** send, double** recv) {
   return DG_OK;
 }
 
+dg_status dg_halo_records(const dg_ctx* c, int64_t* send_gid, int8_t* send_face, int64_t* recv_gid, int8_t* recv_face) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  for (int64_t s = 0; s < c->nsend; ++s) {
+    if (send_gid) send_gid[s] = c->gid[c->send_elem[s]];
+    if (send_face) send_face[s] = int8_t(c->send_face[s]);
+  }
+  for (int64_t g = 0; g < c->nrecv; ++g) {
+    if (recv_gid) recv_gid[g] = c->recv_gid[g];
+    if (recv_face) recv_face[g] = int8_t(c->recv_face[g]);
+  }
+  return DG_OK;
+}
+
 dg_status dg_get_operators(const dg_ctx* c, double* r, double* s, double* t, double* Dr, double* Ds, double* Dt,
                            double* LIFT, int32_t* Fmask) {
   if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");

@@ -39,6 +39,8 @@ struct dg_ctx {
   std::vector<dg_peer> peers;
   std::vector<int32_t> send_elem;   // per send record: internal element
   std::vector<uint8_t> send_face;   // per send record: local face
+  std::vector<int64_t> recv_gid;    // per recv record: sender's global element
+  std::vector<uint8_t> recv_face;   // per recv record: sender's face
   int64_t nsend = 0, nrecv = 0;
 
   // ---- device workspace

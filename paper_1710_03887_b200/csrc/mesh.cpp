@@ -303,6 +303,8 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
       const Ghost& g = rv[i];
       c->nbr[g.l * 4 + g.f] = int32_t(roff + int64_t(i));
       c->code[g.l * 4 + g.f] = uint8_t(32 + g.sface * 6 + g.sigma);
+      c->recv_gid.push_back(g.sgid);
+      c->recv_face.push_back(uint8_t(g.sface));
     }
     P.nrecv = int64_t(rv.size());
     roff += P.nrecv;
