@@ -99,6 +99,19 @@ __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   }
 }
 
+// rho > 0, p > 0 and all five conserved values finite, decided with integer ops on the
+// IEEE bit patterns (keeps the check off the FP64 pipe)
+__device__ __forceinline__ bool state_ok(double rho, double p, double mx, double my, double mz, double E) {
+  const long long r = __double_as_longlong(rho), pp = __double_as_longlong(p);
+  const long long EXP = 0x7ff0000000000000LL;
+  const bool fin = ((__double_as_longlong(mx) & EXP) != EXP) & ((__double_as_longlong(my) & EXP) != EXP) &
+                   ((__double_as_longlong(mz) & EXP) != EXP) & ((__double_as_longlong(E) & EXP) != EXP);
+  // positive, non-zero, finite (NaN and +inf have the exponent all ones)
+  const bool rpos = (r > 0) & ((r & EXP) != EXP);
+  const bool ppos = (pp > 0) & ((pp & EXP) != EXP);
+  return fin & rpos & ppos;
+}
+
 __device__ __forceinline__ void flag_blowup(int* flag, int64_t gid) {
   if (atomicCAS(flag, 0, 1) == 0) flag[1] = (int)gid;
 }
@@ -456,7 +469,10 @@ struct WS {
 #ifndef DG_FACE_BATCH
 #define DG_FACE_BATCH 2
 #endif
-  static constexpr int PW = DG_WS_PW, CW = 8;               // producer / consumer warps
+#ifndef DG_WS_CW
+#define DG_WS_CW 8
+#endif
+  static constexpr int PW = DG_WS_PW, CW = DG_WS_CW;        // producer / consumer warps
   static constexpr int FB = DG_FACE_BATCH;                  // face passes batched per producer iteration
   static constexpr int NT = 32 * (PW + CW);
   static constexpr int PT = 32 * PW, CT = 32 * CW;
@@ -632,6 +648,161 @@ __device__ __forceinline__ void ws_consumer(const ConsumerIO<N, MODE>& io, int c
   if (io.ctid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a0), "d"(b0));
+}
+
+// Balanced work split for the m8 consumer: units are (8-row tile, n-tile pair) (weight 2) and
+// (8-row tile, odd trailing n-tile) (weight 1).  Pairs go round-robin over the consumer warps,
+// singles greedily to the least-loaded SMSP (warp cw runs on SMSP cw % 4); every consumer
+// thread evaluates the same deterministic assignment.
+template <int N>
+struct M8Plan {
+  static constexpr int MT8 = WS<N>::ROWS / 8;
+  static constexpr int NPG = Shape<N>::NTL / 2, HS = Shape<N>::NTL % 2;
+  static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N>::CW;
+  static constexpr int CPMAX = (P + CW - 1) / CW;
+  static constexpr int CSMAX = 4;   // dispatch bound on singles per warp
+};
+
+template <int N>
+__device__ __forceinline__ void m8_singles(int cw, int* out, int& count) {
+  using PL = M8Plan<N>;
+  int load[PL::CW];
+  int smsp[4] = {0, 0, 0, 0};
+  for (int w = 0; w < PL::CW; ++w) {
+    load[w] = 2 * (PL::P > w ? (PL::P - 1 - w) / PL::CW + 1 : 0);
+    smsp[w % 4] += load[w];
+  }
+  count = 0;
+  for (int s = 0; s < PL::SG; ++s) {
+    int best = 0;
+    for (int w = 1; w < PL::CW; ++w) {
+      const int a = smsp[w % 4] * 64 + load[w], b = smsp[best % 4] * 64 + load[best];
+      if (a < b) best = w;
+    }
+    load[best] += 1;
+    smsp[best % 4] += 1;
+    if (best == cw && count < PL::CSMAX) out[count++] = s;
+  }
+}
+
+template <int N, int MODE, int NPAIR, int NSING>
+__device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, int cw, const int* singles) {
+  using S = Shape<N>;
+  using W = WS<N>;
+  using PL = M8Plan<N>;
+  constexpr int NP = S::NP, EB = W::EB, NT = W::NT, XSV = W::XSV, XSF = W::XSF;
+  const StageArgs& A = io.A;
+  const int lane = io.lane, g = lane >> 2, t4 = lane & 3;
+  int mtp[NPAIR > 0 ? NPAIR : 1], ntp[NPAIR > 0 ? NPAIR : 1], mts[NSING > 0 ? NSING : 1];
+#pragma unroll
+  for (int k = 0; k < NPAIR; ++k) {
+    const int p = cw + k * W::CW;
+    mtp[k] = p / PL::NPG;
+    ntp[k] = 2 * (p % PL::NPG);
+  }
+#pragma unroll
+  for (int k = 0; k < NSING; ++k) mts[k] = singles[k];
+  constexpr int NSLOT = 2 * NPAIR + NSING;
+  for (int j = 0; j < io.nmine; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    const int e0 = A.e_begin + tile * EB;
+    const int ne = min(EB, A.e_end - e0);
+    const int buf = j & 1;
+    double* q_s = reinterpret_cast<double*>(io.in0 + buf * W::BIN);
+    double acc[NSLOT > 0 ? NSLOT : 1][2];
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u) acc[u][0] = acc[u][1] = 0.0;
+    auto unit_mt = [&](int u) { return u < 2 * NPAIR ? mtp[u >> 1] : mts[u - 2 * NPAIR]; };
+    auto unit_nt = [&](int u) { return u < 2 * NPAIR ? ntp[u >> 1] + (u & 1) : S::NTL - 1; };
+    auto kloop = [&](auto xblk) {
+      constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
+      if (A.debug & 1) return;
+      const double* X = (K0 == 0) ? io.sXv : io.sXf;
+#pragma unroll KUNROLL
+      for (int ks = K0; ks < K1; ++ks) {
+        const double* ob = io.sOp + ks * S::NTL * 32;
+#pragma unroll
+        for (int k = 0; k < NPAIR; ++k) {
+          const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+          const double2 b = *reinterpret_cast<const double2*>(ob + ntp[k] * 32 + 2 * lane);
+          dmma_8x8x4(acc[2 * k], a0, b.x);
+          dmma_8x8x4(acc[2 * k + 1], a0, b.y);
+        }
+#pragma unroll
+        for (int k = 0; k < NSING; ++k) {
+          const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+          dmma_8x8x4(acc[2 * NPAIR + k], a0, ob[(S::NTL - 1) * 32 + lane]);
+        }
+      }
+    };
+    // residual prefetch (8-row tiles: one row per lane group)
+    double rprev[NSLOT > 0 ? NSLOT : 1][2];
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int row = unit_mt(u) * 8 + g, e = row / 5;
+        const int n = unit_nt(u) * 8 + 2 * t4 + q;
+        const bool ok = MODE == MODE_UPDATE && e < ne && n < NP;
+        rprev[u][q] = ok ? __ldg(A.res + size_t(e0) * 5 * NP + row * NP + n) : 0.0;
+      }
+    if (io.ctid < 32) trace_ev(A, j, 0);
+    nbar_sync(W::BAR_XV_FULL, NT);
+    if (io.ctid < 32) trace_ev(A, j, 1);
+    kloop(KBlk<XSV, 0, S::KSV>{});
+    if (io.ctid < 32) trace_ev(A, j, 2);
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+    nbar_sync(W::BAR_XF_FULL, NT);
+    if (io.ctid < 32) trace_ev(A, j, 3);
+    kloop(KBlk<XSF, S::KSV, S::KS4>{});
+    if (io.ctid < 32) trace_ev(A, j, 4);
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
+    const bool staged = MODE == MODE_UPDATE && ne == EB;
+#pragma unroll
+    for (int u = 0; u < NSLOT; ++u) {
+      const int row = unit_mt(u) * 8 + g;
+      const int e = row / 5, c = row - 5 * (row / 5);
+      if (e >= ne) continue;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int n = unit_nt(u) * 8 + 2 * t4 + q;
+        if (n >= NP) continue;
+        const double rhs = acc[u][q];
+        const int li = row * NP + n;
+        if (MODE == MODE_UPDATE) {
+          const size_t gi = size_t(e0) * 5 * NP + li;
+          const double rr = fma(A.a, rprev[u][q], A.dt * rhs);
+          const double qn = fma(A.b, rr, q_s[li]);
+          A.res[gi] = rr;
+          if (staged) q_s[li] = qn;
+          else A.Qout[gi] = qn;
+        } else {
+          A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
+        }
+      }
+    }
+    if (staged) {
+      nbar_sync(W::BAR_C, W::CT);
+      if (io.ctid == 0) {
+        fence_proxy_async();
+        tma_store_1d(A.Qout + size_t(e0) * 5 * NP, q_s, W::BQ);
+        tma_store_commit_and_wait_read();
+      }
+    }
+    if (io.ctid < 32) trace_ev(A, j, 5);
+    if (j + 2 < io.nmine && io.ctid < 32) {
+      __syncwarp();
+      nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
+    }
+  }
+  if (io.ctid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs A) {
   using S = Shape<N>;
@@ -758,7 +929,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           const double ri = rcp_nr(rho);
           const double u = mx * ri, v = my * ri, w = mz * ri;
           const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-          if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(A.flag, A.gid[e0 + e]);
+          if (!state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
           sRi[idx] = ri;
           sPr[idx] = p;
           sCs[idx] = sqrt_nr(gamma * p * ri);
@@ -800,7 +971,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // node wave speeds; stage 2: face max; stage 3: fluxes and dF.  The passes interleave, so
       // the FP64 latency of one pass hides behind the others.
       if (!(A.debug & 2)) {
-        double rip[FPASS], unp[FPASS], pp[FPASS], lam[FPASS];
+        double rip[FPASS], unp[FPASS], pp[FPASS], lam[FPASS], unmv[FPASS];
 #pragma unroll
         for (int u = 0; u < FPASS; ++u) {
           const int face = pwarp * W::NSEG + u * STRIDE + seg;
@@ -820,6 +991,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
             }
             const double* q = q_s + e * 5 * NP + vn;
             const double unm = (q[NP] * nx + q[2 * NP] * ny + q[3 * NP] * nz) * sRi[vm];
+            unmv[u] = unm;
             rip[u] = rcp_nr(qp[u][0]);
             unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
             pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
@@ -860,7 +1032,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
           // own side from the volume phase's primitives, exterior side from stage 1
           const double pm = sPr[vm];
-          const double unm = (qm[1] * nx + qm[2] * ny + qm[3] * nz) * sRi[vm];
+          const double unm = unmv[u];
           const double pdm = pm - A.pref, pdp = pp[u] - A.pref;
           double df[5];
           df[0] = qm[0] * unm - qp[u][0] * unp[u];
@@ -888,10 +1060,32 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     const int s0 = ((cw - P % W::CW) % W::CW + W::CW) % W::CW;     // first single of this warp
     const int cs = SG > s0 ? (SG - 1 - s0) / W::CW + 1 : 0;
     ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, nmine, DG_PROD_HIGH ? tid : tid - W::PT, lane};
-    if (cp == CPMAX && cs == CSMAX) ws_consumer<N, MODE, CPMAX, CSMAX>(io, cw, s0);
-    else if (cp == CPMAX && cs == CSMAX - 1) ws_consumer<N, MODE, CPMAX, (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
-    else if (cp == CPMAX - 1 && cs == CSMAX) ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), CSMAX>(io, cw, s0);
-    else ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
+#ifndef DG_M8
+#define DG_M8 1
+#endif
+    if (DG_M8) {
+      using PL = M8Plan<N>;
+      int singles[PL::CSMAX], ns = 0;
+      m8_singles<N>(cw, singles, ns);
+      const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
+      constexpr int CP = PL::CPMAX, CPm = PL::CPMAX > 0 ? PL::CPMAX - 1 : 0;
+      // instantiate only the per-warp shapes the greedy plan can produce
+      constexpr int SMAX = (PL::SG + PL::CW - 1) / PL::CW + 1;
+#define DG_M8_CASE(PA, SI)                                                   \
+  if constexpr (SI <= SMAX) {                                                \
+    if (np8 == PA && ns == SI) ws_consumer_m8<N, MODE, PA, SI>(io, cw, singles); \
+  }
+      DG_M8_CASE(CP, 0) DG_M8_CASE(CP, 1) DG_M8_CASE(CP, 2) DG_M8_CASE(CP, 3) DG_M8_CASE(CP, 4)
+      if (CPm != CP) {
+        DG_M8_CASE(CPm, 0) DG_M8_CASE(CPm, 1) DG_M8_CASE(CPm, 2) DG_M8_CASE(CPm, 3) DG_M8_CASE(CPm, 4)
+      }
+#undef DG_M8_CASE
+    } else {
+      if (cp == CPMAX && cs == CSMAX) ws_consumer<N, MODE, CPMAX, CSMAX>(io, cw, s0);
+      else if (cp == CPMAX && cs == CSMAX - 1) ws_consumer<N, MODE, CPMAX, (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
+      else if (cp == CPMAX - 1 && cs == CSMAX) ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), CSMAX>(io, cw, s0);
+      else ws_consumer<N, MODE, (CPMAX > 0 ? CPMAX - 1 : 0), (CSMAX > 0 ? CSMAX - 1 : 0)>(io, cw, s0);
+    }
   }
 }
 
