@@ -912,9 +912,20 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       for (int u = 0; u < FPASS; ++u) {
         const int face = pwarp * W::NSEG + u * STRIDE + seg;
         const int e = face >> 2, f = face & 3;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];    // finite filler for idle lanes
         if (!(A.debug & 2) && lane_ok && face < EB * 4 && e < ne) {
           const int code = c_s[e * 4 + f];
-          if (code < CODE_BC) gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
+          if (code < CODE_BC) {
+            gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
+          } else {   // boundary ghost from the own trace (Q of this tile is in shared memory)
+            const double* G = g_s + e * GEO + 9 + 4 * f;
+            const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+            double qm[5];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+            ghost_trace(A, code - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
+          }
         }
       }
       // ---- volume fluxes -> Xv; own-node 1/rho, p, c -> sRi/sPr/sCs for the face phase
@@ -972,31 +983,24 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // the FP64 latency of one pass hides behind the others.
       if (!(A.debug & 2)) {
         double rip[FPASS], unp[FPASS], pp[FPASS], lam[FPASS], unmv[FPASS];
+        // Stage 1, branch-free: idle lanes work on a clamped (valid) node and are masked below
 #pragma unroll
         for (int u = 0; u < FPASS; ++u) {
           const int face = pwarp * W::NSEG + u * STRIDE + seg;
-          const int e = face >> 2, f = face & 3;
-          lam[u] = 0.0;
-          if (lane_ok && face < EB * 4 && e < ne) {
-            const double* G = g_s + e * GEO + 9 + 4 * f;
-            const double nx = G[0], ny = G[1], nz = G[2];
-            const int vn = sFm[f * NFP + i], vm = e * NP + vn;
-            const int code = c_s[e * 4 + f];
-            if (code >= CODE_BC) {
-              const double* q = q_s + e * 5 * NP + vn;
-              double qm[5];
-#pragma unroll
-              for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
-              ghost_trace(A, code - CODE_BC, qm, nx, ny, nz, qp[u]);
-            }
-            const double* q = q_s + e * 5 * NP + vn;
-            const double unm = (q[NP] * nx + q[2 * NP] * ny + q[3 * NP] * nz) * sRi[vm];
-            unmv[u] = unm;
-            rip[u] = rcp_nr(qp[u][0]);
-            unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
-            pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
-            lam[u] = fmax(fabs(unm) + sCs[vm], fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
-          }
+          const bool act = lane_ok && face < EB * 4 && (face >> 2) < ne;
+          const int fc = act ? face : 0;
+          const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+          const double* G = g_s + e * GEO + 9 + 4 * f;
+          const double nx = G[0], ny = G[1], nz = G[2];
+          const int vn = sFm[f * NFP + ii], vm = e * NP + vn;
+          const double* q = q_s + e * 5 * NP + vn;
+          const double unm = (q[NP] * nx + q[2 * NP] * ny + q[3 * NP] * nz) * sRi[vm];
+          unmv[u] = unm;
+          rip[u] = rcp_nr(qp[u][0]);
+          unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
+          pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
+          const double l = fmax(fabs(unm) + sCs[vm], fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
+          lam[u] = act ? l : 0.0;
         }
         if (A.lambda_mode == 0) {
           // face max over the segment's NFP lanes: inclusive shuffle scans of all passes at once
@@ -1011,21 +1015,17 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 #pragma unroll
           for (int u = 0; u < FPASS; ++u) lam[u] = __shfl_sync(0xffffffffu, lam[u], lane_ok ? seg * NFP + NFP - 1 : lane);
         }
+        // Stage 3, branch-free up to the (predicated) stores
 #pragma unroll
         for (int u = 0; u < FPASS; ++u) {
-          if (pwarp * W::NSEG + u * STRIDE >= EB * 4) break;   // warp-uniform
           const int face = pwarp * W::NSEG + u * STRIDE + seg;
-          const int e = face >> 2, f = face & 3;
-          if (!(lane_ok && face < EB * 4)) continue;
-          double* xd = sXf + (e * 5) * XSF + f * NFP + i;
-          if (e >= ne) {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) xd[c * XSF] = 0.0;
-            continue;
-          }
+          const bool slot = lane_ok && face < EB * 4;
+          const bool act = slot && (face >> 2) < ne;
+          const int fc = slot ? face : 0;
+          const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
           const double* G = g_s + e * GEO + 9 + 4 * f;
-          const double nx = G[0], ny = G[1], nz = G[2], hfs = 0.5 * G[3];
-          const int vn = sFm[f * NFP + i], vm = e * NP + vn;
+          const double nx = G[0], ny = G[1], nz = G[2], hfs = act ? 0.5 * G[3] : 0.0;
+          const int vn = sFm[f * NFP + ii], vm = e * NP + vn;
           const double* q = q_s + e * 5 * NP + vn;
           double qm[5];
 #pragma unroll
@@ -1040,9 +1040,12 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           df[2] = fma(pdm, ny, qm[2] * unm) - fma(pdp, ny, qp[u][2] * unp[u]);
           df[3] = fma(pdm, nz, qm[3] * unm) - fma(pdp, nz, qp[u][3] * unp[u]);
           df[4] = (qm[4] + pm) * unm - (qp[u][4] + pp[u]) * unp[u];
-          // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
+          // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-)); zero for idle elements
+          double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
+          if (slot) {
 #pragma unroll
-          for (int c = 0; c < 5; ++c) xd[c * XSF] = hfs * fma(lam[u], qp[u][c] - qm[c], df[c]);
+            for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam[u], qp[u][c] - qm[c], df[c]) : 0.0;
+          }
         }
       }
       if (ptid < 32) trace_ev(A, j, 14);
