@@ -481,7 +481,9 @@ struct WS {
   static_assert(ROWS % 16 == 0, "rows must fill DMMA m16 tiles");
   // consumer work items: (m-tile, group of <= NTG n-tiles); a consumer warp owns up to IPW items
   static constexpr int NTG = 2;                             // B operand stored as n-tile pairs (+ odd tail)
-  static constexpr int NSEG = 32 / Shape<N>::NFP;           // faces per producer warp-pass
+  // faces per producer warp-pass: one face per power-of-two lane segment (butterfly face max)
+  static constexpr int SEGW = Shape<N>::NFP <= 4 ? 4 : Shape<N>::NFP <= 8 ? 8 : Shape<N>::NFP <= 16 ? 16 : 32;
+  static constexpr int NSEG = 32 / SEGW;
   // X is split into its volume block [ROWS][XSV] and face block [ROWS][XSF];
   // strides == 12 (mod 16) doubles keep the A-fragment loads conflict-free
   static constexpr int XSV = (Shape<N>::KVP + 3) / 16 * 16 + 12;
@@ -725,6 +727,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
 #pragma unroll KUNROLL
       for (int ks = K0; ks < K1; ++ks) {
+#ifdef DG_CSLEEP
+        // experiment: leave FP64 issue slots to the producers during the volume contraction
+        if (K0 == 0 && (ks & 3) == 3) __nanosleep(DG_CSLEEP);
+#endif
         const double* ob = io.sOp + ks * S::NTL * 32;
 #pragma unroll
         for (int k = 0; k < NPAIR; ++k) {
@@ -903,8 +909,8 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ptid < 32) trace_ev(A, j, 9);
       // ---- issue this pwarp's neighbour-trace gathers for the whole tile first: their latency
       //      hides behind the volume phase (one face per NFP-lane segment, FPASS passes)
-      const int seg = lane / NFP, i = lane - seg * NFP;
-      const bool lane_ok = seg < W::NSEG;
+      const int seg = lane / W::SEGW, i = lane - seg * W::SEGW;
+      const bool lane_ok = i < NFP;
       constexpr int STRIDE = W::PW * W::NSEG;
       constexpr int FPASS = (EB * 4 + STRIDE - 1) / STRIDE;
       double qp[FPASS][5];
@@ -1003,17 +1009,17 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           lam[u] = act ? l : 0.0;
         }
         if (A.lambda_mode == 0) {
-          // face max over the segment's NFP lanes: inclusive shuffle scans of all passes at once
+          // face max over the segment's lanes: xor butterfly within the power-of-two segment,
+          // on the integer pipe (positive doubles order like their bit patterns; idle lanes hold 0)
 #pragma unroll
-          for (int d = 1; d < NFP; d <<= 1) {
+          for (int d = 1; d < W::SEGW; d <<= 1) {
 #pragma unroll
             for (int u = 0; u < FPASS; ++u) {
-              const double o = __shfl_up_sync(0xffffffffu, lam[u], d);
-              if (lane_ok && i >= d) lam[u] = fmax(lam[u], o);
+              const long long a = __double_as_longlong(lam[u]);
+              const long long o = __shfl_xor_sync(0xffffffffu, a, d);
+              lam[u] = __longlong_as_double(a > o ? a : o);
             }
           }
-#pragma unroll
-          for (int u = 0; u < FPASS; ++u) lam[u] = __shfl_sync(0xffffffffu, lam[u], lane_ok ? seg * NFP + NFP - 1 : lane);
         }
         // Stage 3, branch-free up to the (predicated) stores
 #pragma unroll
