@@ -746,10 +746,12 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         }
       }
     };
-    // residual prefetch (8-row tiles: one row per lane group)
-    double rprev[NSLOT > 0 ? NSLOT : 1][2];
+    // residual prefetch (8-row tiles: one row per lane group); with few consumer warps the
+    // registers are needed for accumulators and the residual is read in the epilogue instead
+    constexpr bool PREF = W::CW >= 8;
+    double rprev[(NSLOT > 0 && PREF) ? NSLOT : 1][2];
 #pragma unroll
-    for (int u = 0; u < NSLOT; ++u)
+    for (int u = 0; u < (PREF ? NSLOT : 0); ++u)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int row = unit_mt(u) * 8 + g, e = row / 5;
@@ -782,7 +784,8 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         const int li = row * NP + n;
         if (MODE == MODE_UPDATE) {
           const size_t gi = size_t(e0) * 5 * NP + li;
-          const double rr = fma(A.a, rprev[u][q], A.dt * rhs);
+          const double r0 = PREF ? rprev[PREF ? u : 0][q] : (MODE == MODE_UPDATE ? __ldg(A.res + gi) : 0.0);
+          const double rr = fma(A.a, r0, A.dt * rhs);
           const double qn = fma(A.b, rr, q_s[li]);
           A.res[gi] = rr;
           if (staged) q_s[li] = qn;
