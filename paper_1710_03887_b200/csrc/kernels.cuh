@@ -940,38 +940,50 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // ---- volume fluxes -> Xv; own-node 1/rho, p, c -> sRi/sPr/sCs for the face phase
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       if (ptid < 32) trace_ev(A, j, 10);
-      for (int idx = ptid; idx < ((A.debug & 2) ? 0 : EB * NP); idx += PT) {
-        const int e = idx / NP, n = idx - e * NP;
-        double* xr = sXv + (e * 5) * XSV + n;
-        if (e < ne) {
+      // branch-free, two nodes per thread interleaved (independent FP64 chains); slots past the
+      // tile's nodes compute on a clamped node and only store zeros / nothing
+      constexpr int VR = (EB * NP + PT - 1) / PT;
+#pragma unroll
+      for (int r0 = 0; r0 < VR; r0 += 2) {
+        if (A.debug & 2) break;
+#pragma unroll
+        for (int rr = r0; rr < r0 + 2 && rr < VR; ++rr) {
+          const int idx = ptid + rr * PT;
+          const bool inb = idx < EB * NP;
+          const int ic = inb ? idx : 0;
+          const int e = ic / NP, n = ic - e * NP;
+          const bool act = inb && e < ne;
           const double* q = q_s + e * 5 * NP + n;
           const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
           const double ri = rcp_nr(rho);
           const double u = mx * ri, v = my * ri, w = mz * ri;
           const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-          if (!state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
-          sRi[idx] = ri;
-          sPr[idx] = p;
-          sCs[idx] = sqrt_nr(gamma * p * ri);
+          if (act && !state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
+          const double cs = sqrt_nr(gamma * p * ri);
           const double* G = g_s + e * GEO;
           const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
+          double f[3][5];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
             const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
             const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
-            double* xc = xr + d * NP;
-            xc[0] = rho * U;
-            xc[XSV] = fma(cx, pd, mx * U);
-            xc[2 * XSV] = fma(cy, pd, my * U);
-            xc[3 * XSV] = fma(cz, pd, mz * U);
-            xc[4 * XSV] = Ep * U;
+            f[d][0] = rho * U;
+            f[d][1] = fma(cx, pd, mx * U);
+            f[d][2] = fma(cy, pd, my * U);
+            f[d][3] = fma(cz, pd, mz * U);
+            f[d][4] = Ep * U;
           }
-        } else {
+          if (inb) {
+            double* xr = sXv + (e * 5) * XSV + n;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            xr[c * XSV] = 0.0;
-            xr[c * XSV + NP] = 0.0;
-            xr[c * XSV + 2 * NP] = 0.0;
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+              for (int c = 0; c < 5; ++c) xr[c * XSV + d * NP] = act ? f[d][c] : 0.0;
+            if (act) {
+              sRi[idx] = ri;
+              sPr[idx] = p;
+              sCs[idx] = cs;
+            }
           }
         }
       }
