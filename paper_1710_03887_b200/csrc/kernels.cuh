@@ -732,6 +732,17 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         if (K0 == 0 && (ks & 3) == 3) __nanosleep(DG_CSLEEP);
 #endif
         const double* ob = io.sOp + ks * S::NTL * 32;
+#if defined(DG_EXP) && (DG_EXP & 4)
+        // timing experiment only: DMMA with register operands (no shared-memory traffic)
+#pragma unroll
+        for (int k = 0; k < NPAIR; ++k) {
+          dmma_8x8x4(acc[2 * k], 1e-3 * ks, 2e-3);
+          dmma_8x8x4(acc[2 * k + 1], 1e-3 * ks, 3e-3);
+        }
+#pragma unroll
+        for (int k = 0; k < NSING; ++k) dmma_8x8x4(acc[2 * NPAIR + k], 1e-3 * ks, 4e-3);
+        (void)ob; (void)X;
+#else
 #pragma unroll
         for (int k = 0; k < NPAIR; ++k) {
           const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
@@ -744,11 +755,15 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
           dmma_8x8x4(acc[2 * NPAIR + k], a0, ob[(S::NTL - 1) * 32 + lane]);
         }
+#endif
       }
     };
     // residual prefetch (8-row tiles: one row per lane group); with few consumer warps the
     // registers are needed for accumulators and the residual is read in the epilogue instead
-    constexpr bool PREF = W::CW >= 8;
+#ifndef DG_RPREF
+#define DG_RPREF 1
+#endif
+    constexpr bool PREF = DG_RPREF && W::CW >= 8;
     double rprev[(NSLOT > 0 && PREF) ? NSLOT : 1][2];
 #pragma unroll
     for (int u = 0; u < (PREF ? NSLOT : 0); ++u)
@@ -1017,10 +1032,18 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           const double* q = q_s + e * 5 * NP + vn;
           const double unm = (q[NP] * nx + q[2 * NP] * ny + q[3 * NP] * nz) * sRi[vm];
           unmv[u] = unm;
+#if defined(DG_EXP) && (DG_EXP & 1)
+          rip[u] = 0.7;   // timing experiment only
+#else
           rip[u] = rcp_nr(qp[u][0]);
+#endif
           unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
           pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
+#if defined(DG_EXP) && (DG_EXP & 2)
+          const double l = fmax(fabs(unm) + sCs[vm], fabs(unp[u]) + 1.0);   // timing experiment only
+#else
           const double l = fmax(fabs(unm) + sCs[vm], fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
+#endif
           lam[u] = act ? l : 0.0;
         }
         if (A.lambda_mode == 0) {
