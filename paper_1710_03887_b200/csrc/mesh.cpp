@@ -162,7 +162,11 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
     }
   if (mine.empty()) return fail(c, DG_EARG, "rank owns no elements");
   c->K = int64_t(mine.size());
-  c->K_int = int64_t(inter.size());
+  // the interior range ends on a 32-element boundary so that every stage-kernel tile of the
+  // boundary range starts 16-byte aligned for its TMA bulk copies (Q/res: K*5*Np doubles,
+  // geo: 25 doubles, code: 4 bytes per element); the few interior elements moved into the
+  // boundary range merely wait for the halo
+  c->K_int = int64_t(inter.size()) / 32 * 32;
   c->gid = inter;
   c->gid.insert(c->gid.end(), bound.begin(), bound.end());
   std::vector<int64_t> g2l(K, -1), g2pub(K, -1);
