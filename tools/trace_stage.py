@@ -23,11 +23,11 @@ f.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_int]
 f.restype = C.c_int
 assert f(s.ctx, buf, 1024) == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
-names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi",
+names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi", 6: "C eloop", 7: "C barC", 15: "C reswait",
          8: "P start", 9: "P tma", 10: "P XVempty", 11: "P vol", 12: "P fetch", 13: "P XFempty", 14: "P face"}
 t0 = t[2, 0]
 for j in range(2, 8):
     row = t[j]
-    print(f"tile {j}: " + "  ".join(f"{names[e]}={row[e] - t0}" for e in sorted(names)))
+    print(f"tile {j}: " + "  ".join(f"{names[e]}={row[e] - t0}" for e in sorted(names, key=lambda e: row[e])))
 per = (t[10, 0] - t[2, 0]) / 8
 print("cycles per tile (tiles 2..10):", per)
