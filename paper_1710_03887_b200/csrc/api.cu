@@ -73,18 +73,18 @@ int num_sms() {
 
 // ---------------------------------------------------------------- kernel dispatch
 template <int N, int MODE>
-cudaError_t launch_stage_n(const dgk::StageArgs& A, cudaStream_t st) {
-  using T = dgk::Tile<N>;
+cudaError_t launch_ho_n(const dgk::StageArgs& A, cudaStream_t st) {
+  using H = dgk::HO<N>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgk::stage_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(T::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(dgk::stage_ho_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H::SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int ntiles = (A.e_end - A.e_begin + T::EB - 1) / T::EB;
+  const int ntiles = (A.e_end - A.e_begin + H::EB - 1) / H::EB;
   if (ntiles <= 0) return cudaSuccess;
   const int grid = std::min(ntiles, num_sms());
-  dgk::stage_kernel<N, MODE><<<grid, T::NT, T::SMEM, st>>>(A);
+  dgk::stage_ho_kernel<N, MODE><<<grid, H::NT, H::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 
@@ -111,8 +111,8 @@ cudaError_t launch_stage(int N, const dgk::StageArgs& A, cudaStream_t st) {
     case 2: return launch_ws_n<2, MODE>(A, st);
     case 3: return launch_ws_n<3, MODE>(A, st);
     case 4: return launch_ws_n<4, MODE>(A, st);
-    case 5: return launch_stage_n<5, MODE>(A, st);
-    case 6: return launch_stage_n<6, MODE>(A, st);
+    case 5: return launch_ho_n<5, MODE>(A, st);
+    case 6: return launch_ho_n<6, MODE>(A, st);
   }
   return cudaErrorInvalidValue;
 }

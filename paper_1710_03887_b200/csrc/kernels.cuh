@@ -20,9 +20,10 @@
 //      later tiles still read the stage-input state), or rhs written out.
 //
 // stage_ws_kernel (N <= 4) is warp-specialised: 8 producer warps run A-C for
-// tile i+1 while 8 consumer warps run D-E for tile i, handing over the volume
+// tile i+1 while 4-8 consumer warps run D-E for tile i, handing over the volume
 // and face halves of X through named barriers (bar.arrive / bar.sync).
-// stage_kernel (N = 5, 6) runs A-E in lock-step with __syncthreads.
+// stage_ho_kernel (N = 5, 6) runs A-E in phases with all 16 warps and streams Op,
+// too large to keep resident, through a TMA-fed shared-memory ring.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -151,62 +152,6 @@ __device__ __forceinline__ double sqrt_nr(double x) {   // x > 0
   return x * y;
 }
 
-// ---------------------------------------------------------------- pointwise pieces
-// Volume flux at one node: q -> 15 contravariant flux values in X rows e*5+c, cols d*NP+n.
-template <int NP, int XS>
-__device__ __forceinline__ void volume_node(const double* q, const double* G, double* xr, double gm1, double pref,
-                                            int* flag, int64_t gid) {
-  const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
-  const double ri = rcp_nr(rho);
-  const double u = mx * ri, v = my * ri, w = mz * ri;
-  const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-  if (!(rho > 0.0) || !(p > 0.0) || !isfinite(E + mx + my + mz)) flag_blowup(flag, gid);
-  const double Ep = E + p;
-  const double pd = p - pref;   // background-flux subtraction (A14)
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
-    const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
-    double* xc = xr + d * NP;
-    xc[0] = rho * U;
-    xc[XS] = fma(cx, pd, mx * U);
-    xc[2 * XS] = fma(cy, pd, my * U);
-    xc[3 * XS] = fma(cz, pd, mz * U);
-    xc[4 * XS] = Ep * U;
-  }
-}
-
-// Exterior trace q+ of face node i of face f: neighbour (local / halo) or boundary ghost.
-template <int NP, int NFP>
-__device__ __forceinline__ void exterior_trace(const StageArgs& A, int code, int nb, int f, int i, const uint8_t* tbl,
-                                               const uint8_t* tblf, const double (&qm)[5], double nx, double ny,
-                                               double nz, double (&qp)[5]) {
-  if (code < CODE_GHOST) {
-    const double* q2 = A.Qin + size_t(nb) * 5 * NP + tbl[(f * 24 + code) * NFP + i];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NP);
-  } else if (code < CODE_BC) {
-    const double* q2 = A.recv + size_t(nb) * 5 * NFP + tblf[(f * 24 + code - CODE_GHOST) * NFP + i];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) qp[c] = __ldg(q2 + c * NFP);
-  } else {
-    const int tag = code - CODE_BC;
-    if (tag == 1) {  // reflective wall, Eq. 4 read as a mirror (A2)
-      const double mn = qm[1] * nx + qm[2] * ny + qm[3] * nz;
-      qp[0] = qm[0];
-      qp[1] = qm[1] - 2.0 * mn * nx;
-      qp[2] = qm[2] - 2.0 * mn * ny;
-      qp[3] = qm[3] - 2.0 * mn * nz;
-      qp[4] = qm[4];
-    } else if (tag == 2) {  // pass-through: ambient state of Eq. 3
-#pragma unroll
-      for (int c = 0; c < 5; ++c) qp[c] = A.qinf[c];
-    } else {  // inflow, Eqs. 5-7
-      inflow_state(A.t, A.inflow_alpha, A.gamma, qp);
-    }
-  }
-}
-
 // Neighbour trace for a paired face (local element or halo record); boundary faces are filled later.
 template <int NP, int NFP>
 __device__ __forceinline__ void gather_trace(const StageArgs& A, int code, int nb, int f, int i, const uint8_t* tbl,
@@ -237,188 +182,6 @@ __device__ __forceinline__ void ghost_trace(const StageArgs& A, int tag, const d
     for (int c = 0; c < 5; ++c) qp[c] = A.qinf[c];
   } else {
     inflow_state(A.t, A.inflow_alpha, A.gamma, qp);
-  }
-}
-
-struct SideFlux {
-  double f[5];   // n.F(q) with the ambient pressure subtracted (A14)
-  double speed;  // |u.n| + c
-};
-
-__device__ __forceinline__ SideFlux side_flux(const double (&q)[5], double nx, double ny, double nz, double gamma,
-                                              double pref) {
-  SideFlux s;
-  const double ri = rcp_nr(q[0]);
-  const double un = (q[1] * nx + q[2] * ny + q[3] * nz) * ri;
-  const double p = (gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) * ri);
-  const double pd = p - pref;
-  s.f[0] = q[0] * un;
-  s.f[1] = fma(pd, nx, q[1] * un);
-  s.f[2] = fma(pd, ny, q[2] * un);
-  s.f[3] = fma(pd, nz, q[3] * un);
-  s.f[4] = (q[4] + p) * un;
-  s.speed = fabs(un) + sqrt_nr(gamma * p * ri);
-  return s;
-}
-
-// ---------------------------------------------------------------- lock-step kernel (N = 5, 6)
-template <int N>
-struct Tile {
-  static constexpr int EB = (N <= 3) ? 32 : (N == 4 ? 16 : 8);
-  static constexpr int NT = 512;
-  static constexpr int ROWS = (5 * EB + 15) / 16 * 16;
-  static constexpr int MT = ROWS / 16;
-  static constexpr bool OP_SMEM = Shape<N>::OPN * 8 <= 72 * 1024;
-  static constexpr int NTG = (Shape<N>::NTL >= 4) ? 2 : 1;
-  static constexpr int NGRP = (Shape<N>::NTL + NTG - 1) / NTG;
-  static constexpr int ITEMS = MT * NGRP;
-  static constexpr size_t SMEM_X = size_t(ROWS) * Shape<N>::XS * 8;
-  static constexpr size_t SMEM_OP = OP_SMEM ? size_t(Shape<N>::OPN) * 8 : 0;
-  static constexpr size_t SMEM_Q = size_t(EB) * 5 * Shape<N>::NP * 8;
-  static constexpr size_t SMEM_G = size_t(EB) * GEO * 8;
-  static constexpr size_t SMEM_L = size_t(EB) * 4 * Shape<N>::NFP * 8;
-  static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_X + SMEM_OP + SMEM_Q + SMEM_G + SMEM_L + SMEM_T;
-  static_assert(SMEM <= 227 * 1024, "tile does not fit in shared memory");
-};
-
-template <int N, int MODE>
-__global__ void __launch_bounds__(Tile<N>::NT, 1) stage_kernel(const StageArgs A) {
-  using S = Shape<N>;
-  using T = Tile<N>;
-  constexpr int NP = S::NP, NFP = S::NFP, EB = T::EB, NT = T::NT, XS = S::XS;
-  extern __shared__ __align__(128) unsigned char smem[];
-  double* sX = reinterpret_cast<double*>(smem);
-  double* sOp = sX + T::ROWS * XS;
-  double* sQ = sOp + (T::OP_SMEM ? S::OPN : 0);
-  double* sG = sQ + EB * 5 * NP;
-  double* sL = sG + EB * GEO;
-  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sL + EB * 4 * NFP);
-  uint8_t* sTblf = sTbl + 96 * NFP;
-  uint8_t* sFm = sTblf + 96 * NFP;
-  const int tid = threadIdx.x;
-  const double* __restrict__ Op = T::OP_SMEM ? sOp : A.op;
-
-  if (T::OP_SMEM)
-    for (int i = tid; i < S::OPN; i += NT) sOp[i] = A.op[i];
-  for (int i = tid; i < 96 * NFP; i += NT) {
-    sTbl[i] = A.tbl[i];
-    sTblf[i] = A.tblf[i];
-  }
-  for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
-  for (int i = tid; i < T::ROWS * XS; i += NT) sX[i] = 0.0;   // padding rows/columns stay 0
-
-  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
-  const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int e0 = A.e_begin + tile * EB;
-    const int ne = min(EB, A.e_end - e0);
-    __syncthreads();  // previous tile fully consumed
-    {
-      const double* src = A.Qin + size_t(e0) * 5 * NP;
-      const int n = ne * 5 * NP;
-      for (int i = tid; i < n; i += NT) sQ[i] = __ldg(src + i);
-      for (int i = n + tid; i < EB * 5 * NP; i += NT) sQ[i] = 0.0;
-      const double* g = A.geo + size_t(e0) * GEO;
-      for (int i = tid; i < ne * GEO; i += NT) sG[i] = __ldg(g + i);
-    }
-    __syncthreads();
-    for (int idx = tid; idx < ne * NP; idx += NT) {
-      const int e = idx / NP, n = idx - e * NP;
-      volume_node<NP, XS>(sQ + e * 5 * NP + n, sG + e * GEO, sX + (e * 5) * XS + n, gm1, A.pref, A.flag, A.gid[e0 + e]);
-    }
-    constexpr int FN = EB * 4 * NFP;
-    constexpr int FR = (FN + NT - 1) / NT;
-    double qm[FR][5], qp[FR][5];
-#pragma unroll
-    for (int r = 0; r < FR; ++r) {
-      const int idx = tid + r * NT;
-      if (idx >= FN) continue;
-      const int e = idx / (4 * NFP), fi = idx - e * 4 * NFP, f = fi / NFP, i = fi - f * NFP;
-      if (e >= ne) {
-        sL[idx] = 0.0;
-        continue;
-      }
-      const double* q = sQ + e * 5 * NP + sFm[fi];
-#pragma unroll
-      for (int c = 0; c < 5; ++c) qm[r][c] = q[c * NP];
-      const int ke = e0 + e;
-      const double* G = sG + e * GEO + 9 + 4 * f;
-      exterior_trace<NP, NFP>(A, A.code[ke * 4 + f], A.nbr[ke * 4 + f], f, i, sTbl, sTblf, qm[r], G[0], G[1], G[2], qp[r]);
-      const SideFlux sm = side_flux(qm[r], G[0], G[1], G[2], gamma, A.pref);
-      const SideFlux sp = side_flux(qp[r], G[0], G[1], G[2], gamma, A.pref);
-      sL[idx] = fmax(sm.speed, sp.speed);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < FR; ++r) {
-      const int idx = tid + r * NT;
-      if (idx >= FN) continue;
-      const int e = idx / (4 * NFP), fi = idx - e * 4 * NFP, f = fi / NFP;
-      double* xd = sX + (e * 5) * XS + S::KVP + fi;
-      if (e >= ne) continue;
-      double lam;
-      if (A.lambda_mode == 0) {
-        const double* l = sL + e * 4 * NFP + f * NFP;
-        lam = l[0];
-#pragma unroll
-        for (int j = 1; j < NFP; ++j) lam = fmax(lam, l[j]);
-      } else {
-        lam = sL[idx];
-      }
-      const double* G = sG + e * GEO + 9 + 4 * f;
-      const SideFlux sm = side_flux(qm[r], G[0], G[1], G[2], gamma, A.pref);
-      const SideFlux sp = side_flux(qp[r], G[0], G[1], G[2], gamma, A.pref);
-#pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        const double fstar = 0.5 * (sm.f[c] + sp.f[c]) - 0.5 * lam * (qp[r][c] - qm[r][c]);
-        xd[c * XS] = G[3] * (sm.f[c] - fstar);
-      }
-    }
-    __syncthreads();
-    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-    for (int item = warp; item < T::ITEMS; item += NT / 32) {
-      const int mt = item / T::NGRP, ng = item - mt * T::NGRP;
-      double acc[T::NTG][4];
-#pragma unroll
-      for (int j = 0; j < T::NTG; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-      const double* xa = sX + (mt * 16 + g) * XS + t4;
-      const double* ob = Op + lane;
-#pragma unroll 4
-      for (int ks = 0; ks < S::KS4; ++ks) {
-        const double a0 = xa[ks * 4], a1 = xa[8 * XS + ks * 4];
-#pragma unroll
-        for (int j = 0; j < T::NTG; ++j) {
-          const int nt = ng * T::NTG + j;
-          if (nt < S::NTL) dmma_16x8x4(acc[j], a0, a1, ob[(ks * S::NTL + nt) * 32]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < T::NTG; ++j) {
-        const int nt = ng * T::NTG + j;
-        if (nt >= S::NTL) continue;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = mt * 16 + g + 8 * h;
-          const int e = row / 5, c = row - 5 * (row / 5);
-          if (e >= ne) continue;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int n = nt * 8 + 2 * t4 + q;
-            if (n >= NP) continue;
-            const double rhs = acc[j][2 * h + q];
-            if (MODE == MODE_UPDATE) {
-              const size_t gi = (size_t(e0 + e) * 5 + c) * NP + n;
-              const double rr = A.a * A.res[gi] + A.dt * rhs;
-              A.res[gi] = rr;
-              A.Qout[gi] = sQ[(e * 5 + c) * NP + n] + A.b * rr;
-            } else {
-              A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
-            }
-          }
-        }
-      }
-    }
   }
 }
 
@@ -759,20 +522,8 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);   // [0,1] inputs, [2] residual
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // B operand regrouped per k-step: n-tile pairs with a lane's two values adjacent, then the
-  // odd trailing n-tile compacted to its real columns
-  for (int i = tid; i < W::OPC; i += NT) {
-    const int ks = i / W::OPW, r = i - ks * W::OPW;
-    int ln, nt;
-    if (r < W::NPG * 64) {
-      ln = (r & 63) >> 1;
-      nt = 2 * (r >> 6) + (r & 1);
-    } else {
-      ln = r - W::NPG * 64;
-      nt = S::NTL - 1;
-    }
-    sOp[i] = A.op[(ks * S::NTL + nt) * 32 + ln];
-  }
+  // B operand (mesh.cpp layout: per k-step the n-tile pairs, then the compacted odd n-tile)
+  for (int i = tid; i < W::OPC; i += NT) sOp[i] = A.op[i];
   for (int i = tid; i < 96 * NFP; i += NT) {
     sTbl[i] = A.tbl[i];
     sTblf[i] = A.tblf[i];
@@ -1016,6 +767,393 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     }
 #undef DG_M8_CASE
   }
+}
+
+// ---------------------------------------------------------------- high-order kernel (N = 5, 6)
+// For N = 5, 6 the contraction is ~90 % of the stage's flops and the operator Op (113 KB /
+// 256 KB) does not fit next to the tile, so the warp specialisation of the N <= 4 kernel buys
+// little.  All 16 warps run each tile in phases -- traces, volume and face fluxes into X, the
+// contraction, the LSERK epilogue -- while Op streams through a 3-slot shared-memory ring in
+// chunks of KC k-steps (TMA bulk copies, full/empty mbarriers, prefetched two chunks ahead and
+// across tile boundaries), and the next tile's inputs arrive by TMA during the current tile.
+// Each warp owns one work item: an n-tile pair (or the compacted odd n-tile) times up to MU
+// consecutive 8-row tiles, so every B fragment is read once per k-step and reused MU times;
+// items go to SMSPs longest-first to balance the per-SMSP FP64 pipes.
+template <int N>
+struct HO {
+  using S = Shape<N>;
+  static constexpr int EB = 8, NW = 16, NT = 32 * NW;
+  static constexpr int ROWS = 5 * EB, MT8 = ROWS / 8;
+  static constexpr int XS = S::XS;
+  static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
+  static constexpr int GS = HS ? S::NP - 8 * (S::NTL - 1) : 0;
+  static constexpr int OPW = NPG * 64 + 4 * GS;                   // doubles per k-step of Op
+  static constexpr int KC = (N == 6) ? 6 : 7;                     // k-steps per ring chunk
+  static constexpr int NCH = (S::KS4 + KC - 1) / KC;
+  static constexpr uint32_t BCH = uint32_t(KC) * OPW * 8;
+  static constexpr int MU = (N == 6) ? 3 : 2;                     // 8-row tiles per work item
+  static constexpr int SEGW = S::NFP <= 4 ? 4 : S::NFP <= 8 ? 8 : S::NFP <= 16 ? 16 : 32;
+  static constexpr int NSEG = 32 / SEGW, STRIDE = NW * NSEG;
+  static constexpr int FPASS = (EB * 4 + STRIDE - 1) / STRIDE;
+  static constexpr uint32_t BQ = uint32_t(EB) * 5 * S::NP * 8;
+  static constexpr uint32_t BG = uint32_t(EB) * GEO * 8;
+  static constexpr uint32_t BN = uint32_t(EB) * 4 * 4;
+  static constexpr uint32_t BC = uint32_t(EB) * 4;
+  static constexpr uint32_t BIN = BQ + BG + BN + BC;
+  static_assert(BQ % 16 == 0 && BG % 16 == 0 && BCH % 16 == 0 && (uint32_t(OPW) * 8) % 16 == 0, "TMA sizes");
+  static constexpr size_t SMEM_X = size_t(ROWS) * XS * 8;
+  static_assert(2 * size_t(BQ) <= SMEM_X, "X doubles as the output staging tile");
+  static constexpr size_t SMEM_T = size_t(2 * 96 * S::NFP + 4 * S::NFP + 15) / 16 * 16;
+  static constexpr size_t SMEM = SMEM_X + 2 * size_t(BIN) + 3 * size_t(BCH) + SMEM_T + 64;
+  static_assert(SMEM <= 227 * 1024, "high-order tile does not fit in shared memory");
+};
+
+struct HOItem {
+  int kind, p, m0, mc;   // kind 0: n-tile pair p; 1: odd n-tile; -1: idle
+};
+
+// Deterministic plan, evaluated by every thread: items (n-group x runs of <= MU row tiles) in
+// creation order, placed longest-first on the least-loaded SMSP (warp w runs on SMSP w % 4).
+template <int N>
+__device__ __forceinline__ HOItem ho_plan(int warp) {
+  using H = HO<N>;
+  constexpr int NG = H::NPG + H::HS, NRUN = (H::MT8 + H::MU - 1) / H::MU, NIT = NG * NRUN;
+  static_assert(NIT <= H::NW, "more work items than warps");
+  int load[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  HOItem mine{-1, 0, 0, 0};
+  for (int wgt = 2 * H::MU; wgt >= 1; --wgt)
+    for (int it = 0; it < NIT; ++it) {
+      const int grp = it / NRUN, run = it % NRUN;
+      const int kind = grp < H::NPG ? 0 : 1;
+      const int m0 = run * H::MU, mc = min(H::MU, H::MT8 - m0);
+      if ((kind == 0 ? 2 : 1) * mc != wgt) continue;
+      int best = -1;
+      for (int s = 0; s < 4; ++s)
+        if (cnt[s] < H::NW / 4 && (best < 0 || load[s] < load[best])) best = s;
+      const int w = best + 4 * cnt[best];
+      ++cnt[best];
+      load[best] += wgt;
+      if (w == warp) mine = HOItem{kind, kind == 0 ? grp : 0, m0, mc};
+    }
+  return mine;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs A) {
+  using S = Shape<N>;
+  using H = HO<N>;
+  constexpr int NP = S::NP, NFP = S::NFP, EB = H::EB, NT = H::NT, XS = H::XS, MU = H::MU;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sX = reinterpret_cast<double*>(smem);
+  unsigned char* in0 = smem + H::SMEM_X;
+  double* ring = reinterpret_cast<double*>(in0 + 2 * H::BIN);
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(ring) + 3 * H::BCH;
+  uint8_t* sTblf = sTbl + 96 * NFP;
+  uint8_t* sFm = sTblf + 96 * NFP;
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + H::SMEM_T);   // [0,1] inputs, [2..4] full, [5..7] empty
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  auto bufQ = [&](int b) { return reinterpret_cast<double*>(in0 + b * H::BIN); };
+  auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * H::BIN + H::BQ); };
+  auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * H::BIN + H::BQ + H::BG); };
+  auto bufC = [&](int b) { return reinterpret_cast<uint8_t*>(in0 + b * H::BIN + H::BQ + H::BG + H::BN); };
+
+  for (int i = tid; i < 96 * NFP; i += NT) {
+    sTbl[i] = A.tbl[i];
+    sTblf[i] = A.tblf[i];
+  }
+  for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
+  for (int i = tid; i < H::ROWS * XS; i += NT) sX[i] = 0.0;   // padding columns stay 0
+  if (tid == 0) {
+    for (int b = 0; b < 5; ++b) mbar_init(&sBar[b], 1);
+    for (int b = 5; b < 8; ++b) mbar_init(&sBar[b], H::NW);
+  }
+  __syncthreads();
+
+  const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
+  const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const long long nchunks = (long long)nmine * H::NCH;
+  auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB; };
+  auto is_full = [&](int jj) { return A.e_end - tile_e0(jj) >= EB; };
+  auto fetch = [&](int jj) {   // one thread
+    const int e0 = tile_e0(jj), b = jj & 1;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&sBar[b], H::BIN);
+    tma_load_1d(bufQ(b), A.Qin + size_t(e0) * 5 * NP, H::BQ, &sBar[b]);
+    tma_load_1d(bufG(b), A.geo + size_t(e0) * GEO, H::BG, &sBar[b]);
+    tma_load_1d(bufN(b), A.nbr + size_t(e0) * 4, H::BN, &sBar[b]);
+    tma_load_1d(bufC(b), A.code + size_t(e0) * 4, H::BC, &sBar[b]);
+  };
+  auto load_chunk = [&](long long gc) {   // one thread; the slot is free
+    const int s = int(gc % 3), c = int(gc % H::NCH);
+    const int kc = min(H::KC, S::KS4 - c * H::KC);
+    const uint32_t bytes = uint32_t(kc) * H::OPW * 8;
+    mbar_arrive_expect_tx(&sBar[2 + s], bytes);
+    tma_load_1d(ring + size_t(s) * (H::BCH / 8), A.op + size_t(c) * H::KC * H::OPW, bytes, &sBar[2 + s]);
+  };
+  if (tid == 0 && nmine > 0) {
+    if (is_full(0)) fetch(0);
+    for (long long gc = 0; gc < 2 && gc < nchunks; ++gc) load_chunk(gc);
+  }
+  const HOItem it = ho_plan<N>(warp);
+  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+  long long gch = 0;   // chunks consumed so far
+
+  for (int j = 0; j < nmine; ++j) {
+    const int e0 = tile_e0(j);
+    const int ne = min(EB, A.e_end - e0);
+    const bool full = ne == EB;
+    const int buf = j & 1;
+    double* q_s = bufQ(buf);
+    double* g_s = bufG(buf);
+    int* n_s = bufN(buf);
+    uint8_t* c_s = bufC(buf);
+    if (tid == 0 && j + 1 < nmine && is_full(j + 1)) fetch(j + 1);   // its buffer was freed by tile j-1
+    if (full) {
+      mbar_wait(&sBar[buf], (j >> 1) & 1);
+    } else {   // the last tile: plain loads, zero-filled
+      for (int i = tid; i < EB * 5 * NP; i += NT) q_s[i] = i < ne * 5 * NP ? __ldg(A.Qin + size_t(e0) * 5 * NP + i) : 0.0;
+      for (int i = tid; i < EB * GEO; i += NT) g_s[i] = i < ne * GEO ? __ldg(A.geo + size_t(e0) * GEO + i) : 0.0;
+      for (int i = tid; i < EB * 4; i += NT) {
+        n_s[i] = i < ne * 4 ? __ldg(A.nbr + size_t(e0) * 4 + i) : 0;
+        c_s[i] = i < ne * 4 ? A.code[size_t(e0) * 4 + i] : uint8_t(CODE_BC + 2);
+      }
+      __syncthreads();
+    }
+    // ---- neighbour traces (one face per SEGW-lane segment, FPASS passes)
+    const int seg = lane / H::SEGW, i = lane - seg * H::SEGW;
+    const bool lane_ok = i < NFP;
+    double qp[H::FPASS][5];
+#pragma unroll
+    for (int u = 0; u < H::FPASS; ++u) {
+      const int face = warp * H::NSEG + u * H::STRIDE + seg;
+      const int e = face >> 2, f = face & 3;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
+      if (!(A.debug & 2) && lane_ok && face < EB * 4 && e < ne) {
+        const int code = c_s[e * 4 + f];
+        if (code < CODE_BC) {
+          gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
+        } else {
+          const double* Gf = g_s + e * GEO + 9 + 4 * f;
+          const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+          double qm[5];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+          ghost_trace(A, code - CODE_BC, qm, Gf[0], Gf[1], Gf[2], qp[u]);
+        }
+      }
+    }
+    // the previous tile's output bulk stores have left X
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncthreads();
+    // ---- volume fluxes -> X[:, 0:3Np)
+    if (!(A.debug & 2)) {
+      constexpr int VR = (EB * NP + NT - 1) / NT;
+#pragma unroll
+      for (int rr = 0; rr < VR; ++rr) {
+        const int idx = tid + rr * NT;
+        if (idx >= ne * NP) break;
+        const int e = idx / NP, n = idx - e * NP;
+        const double* q = q_s + e * 5 * NP + n;
+        const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
+        const double ri = rcp_nr(rho);
+        const double u = mx * ri, v = my * ri, w = mz * ri;
+        const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
+        if (!state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
+        const double* Gv = g_s + e * GEO;
+        const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
+        double* xr = sX + (e * 5) * XS + n;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double cx = Gv[3 * d], cy = Gv[3 * d + 1], cz = Gv[3 * d + 2];
+          const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
+          xr[d * NP] = rho * U;
+          xr[XS + d * NP] = fma(cx, pd, mx * U);
+          xr[2 * XS + d * NP] = fma(cy, pd, my * U);
+          xr[3 * XS + d * NP] = fma(cz, pd, mz * U);
+          xr[4 * XS + d * NP] = Ep * U;
+        }
+      }
+    }
+    // ---- face terms -> X[:, KVP:KVP+4Nfp)
+    if (!(A.debug & 2)) {
+      double rip[H::FPASS], unp[H::FPASS], pp[H::FPASS], lam[H::FPASS], unmv[H::FPASS], pmv[H::FPASS];
+#pragma unroll
+      for (int u = 0; u < H::FPASS; ++u) {
+        const int face = warp * H::NSEG + u * H::STRIDE + seg;
+        const bool act = lane_ok && face < EB * 4 && (face >> 2) < ne;
+        const int fc = act ? face : 0;
+        const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+        const double* Gf = g_s + e * GEO + 9 + 4 * f;
+        const double nx = Gf[0], ny = Gf[1], nz = Gf[2];
+        const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
+        const double qm0 = q[0], qm1 = q[NP], qm2 = q[2 * NP], qm3 = q[3 * NP], qm4 = q[4 * NP];
+        const double rim = rcp_nr(qm0);
+        const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
+        const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
+        unmv[u] = unm;
+        pmv[u] = pm;
+        rip[u] = rcp_nr(qp[u][0]);
+        unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
+        pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
+        const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
+        lam[u] = act ? l : 0.0;
+      }
+      if (A.lambda_mode == 0) {
+#pragma unroll
+        for (int d = 1; d < H::SEGW; d <<= 1) {
+#pragma unroll
+          for (int u = 0; u < H::FPASS; ++u) {
+            const long long a = __double_as_longlong(lam[u]);
+            const long long o = __shfl_xor_sync(0xffffffffu, a, d);
+            lam[u] = __longlong_as_double(a > o ? a : o);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < H::FPASS; ++u) {
+        const int face = warp * H::NSEG + u * H::STRIDE + seg;
+        const bool act = lane_ok && face < EB * 4 && (face >> 2) < ne;
+        if (!act) continue;
+        const int e = face >> 2, f = face & 3;
+        const double* Gf = g_s + e * GEO + 9 + 4 * f;
+        const double nx = Gf[0], ny = Gf[1], nz = Gf[2], hfs = 0.5 * Gf[3];
+        const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+        double qm[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+        const double pm = pmv[u], unm = unmv[u];
+        const double pdm = pm - A.pref, pdp = pp[u] - A.pref;
+        double df[5];
+        df[0] = qm[0] * unm - qp[u][0] * unp[u];
+        df[1] = fma(pdm, nx, qm[1] * unm) - fma(pdp, nx, qp[u][1] * unp[u]);
+        df[2] = fma(pdm, ny, qm[2] * unm) - fma(pdp, ny, qp[u][2] * unp[u]);
+        df[3] = fma(pdm, nz, qm[3] * unm) - fma(pdp, nz, qp[u][3] * unp[u]);
+        df[4] = (qm[4] + pm) * unm - (qp[u][4] + pp[u]) * unp[u];
+        // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
+        double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) xd[c * XS] = hfs * fma(lam[u], qp[u][c] - qm[c], df[c]);
+      }
+    }
+    // residual for the epilogue (its latency hides behind the contraction)
+    double rprev[MU][2][2];
+#pragma unroll
+    for (int m = 0; m < MU; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int row = (it.m0 + m) * 8 + g;
+          const int n = (it.kind == 0 ? (2 * it.p + h) * 8 : (S::NTL - 1) * 8) + 2 * t4 + q;
+          const bool ok = MODE == MODE_UPDATE && it.kind >= 0 && m < it.mc && (it.kind == 0 || h == 0) && n < NP &&
+                          row / 5 < ne;
+          rprev[m][h][q] = ok ? __ldg(A.res + size_t(e0) * 5 * NP + row * NP + n) : 0.0;
+        }
+    __syncthreads();   // X complete
+    // ---- contraction: Op streams through the ring, chunk by chunk
+    double acc[MU][2][2];
+#pragma unroll
+    for (int m = 0; m < MU; ++m) acc[m][0][0] = acc[m][0][1] = acc[m][1][0] = acc[m][1][1] = 0.0;
+    const double* xa = sX + (it.m0 * 8 + g) * XS + t4;
+    for (int c = 0; c < H::NCH; ++c) {
+      const long long gc = gch + c;
+      const int s = int(gc % 3);
+      mbar_wait(&sBar[2 + s], uint32_t((gc / 3) & 1));
+      const double* ob = ring + size_t(s) * (H::BCH / 8);
+      const int kc = min(H::KC, S::KS4 - c * H::KC);
+      if (!(A.debug & 1)) {
+        if (it.kind == 0) {
+#pragma unroll
+          for (int kk = 0; kk < H::KC; ++kk) {
+            if (kk < kc) {
+              const double2 b = *reinterpret_cast<const double2*>(ob + kk * H::OPW + it.p * 64 + 2 * lane);
+              const int kcol = (c * H::KC + kk) * 4;
+#pragma unroll
+              for (int m = 0; m < MU; ++m)
+                if (m < it.mc) {
+                  const double a = xa[m * 8 * XS + kcol];
+                  dmma_8x8x4(acc[m][0], a, b.x);
+                  dmma_8x8x4(acc[m][1], a, b.y);
+                }
+            }
+          }
+        } else if (it.kind == 1) {
+#pragma unroll
+          for (int kk = 0; kk < H::KC; ++kk) {
+            if (kk < kc) {
+              const double b = lane < 4 * H::GS ? ob[kk * H::OPW + H::NPG * 64 + lane] : 0.0;
+              const int kcol = (c * H::KC + kk) * 4;
+#pragma unroll
+              for (int m = 0; m < MU; ++m)
+                if (m < it.mc) dmma_8x8x4(acc[m][0], xa[m * 8 * XS + kcol], b);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sBar[5 + s]);
+      // loader: chunk gc+2 goes into the slot chunk gc-1 used (all warps have released it)
+      if (tid == 0 && gc + 2 < nchunks) {
+        const long long gn = gc + 2;
+        if (gn >= 3) mbar_wait(&sBar[5 + int(gn % 3)], uint32_t(((gn / 3) - 1) & 1));
+        load_chunk(gn);
+      }
+      __syncwarp();
+    }
+    gch += H::NCH;
+    __syncthreads();   // every read of X done: it becomes the output staging tile
+    // ---- epilogue
+    const bool staged = MODE == MODE_UPDATE && full;
+    double* sres = sX;
+    double* sq = sX + EB * 5 * NP;
+    if (it.kind >= 0) {
+#pragma unroll
+      for (int m = 0; m < MU; ++m) {
+        if (m >= it.mc) continue;
+        const int row = (it.m0 + m) * 8 + g;
+        const int e = row / 5, cf = row - 5 * (row / 5);
+        if (e >= ne) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (it.kind == 1 && h == 1) continue;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = (it.kind == 0 ? (2 * it.p + h) * 8 : (S::NTL - 1) * 8) + 2 * t4 + q;
+            if (n >= NP) continue;
+            const int li = row * NP + n;
+            const double rhs = acc[m][h][q];
+            if (MODE == MODE_UPDATE) {
+              const double rr = fma(A.a, rprev[m][h][q], A.dt * rhs);
+              const double qn = fma(A.b, rr, q_s[li]);
+              if (staged) {
+                sres[li] = rr;
+                sq[li] = qn;
+              } else {
+                const size_t gi = size_t(e0) * 5 * NP + li;
+                A.res[gi] = rr;
+                A.Qout[gi] = qn;
+              }
+            } else {
+              A.out[(size_t(cf) * A.Kpub + A.pub[e0 + e]) * NP + n] = rhs;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();   // staging complete; q_s of this tile no longer read
+    if (tid == 0 && staged) {
+      fence_proxy_async();
+      tma_store_1d(A.res + size_t(e0) * 5 * NP, sres, H::BQ);
+      tma_store_1d(A.Qout + size_t(e0) * 5 * NP, sq, H::BQ);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // pack the traces of this rank's partition faces: send[s][c][j] = Q[k][c][Fmask_f[j]]

@@ -353,13 +353,21 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
     if (k < KVP) return 0.0;
     return c->ref.LIFT[n * 4 * Nfp + (k - KVP)];
   };
-  c->opfrag.assign(size_t(KS4) * NTL * 32, 0.0);
-  for (int ks = 0; ks < KS4; ++ks)
-    for (int nt = 0; nt < NTL; ++nt)
-      for (int lane = 0; lane < 32; ++lane) {
-        int g = lane >> 2, t = lane & 3;
-        c->opfrag[(size_t(ks) * NTL + nt) * 32 + lane] = op(8 * nt + g, 4 * ks + t);
-      }
+  // per k-step (OPW doubles, one contiguous block so the kernels can stream it in chunks):
+  // NPG n-tile pairs of 64 doubles, lane l holding B(4ks+l%4, 8(2p)+l/4) and B(.., 8(2p+1)+l/4)
+  // adjacent; then, for odd NTL, the trailing n-tile compacted to the lanes of its GS real
+  // columns (l < 4 GS)
+  const int NPG = NTL / 2, GS = (NTL % 2) ? Np - 8 * (NTL - 1) : 0, OPW = NPG * 64 + 4 * GS;
+  c->opfrag.assign(size_t(KS4) * OPW, 0.0);
+  for (int ks = 0; ks < KS4; ++ks) {
+    double* o = c->opfrag.data() + size_t(ks) * OPW;
+    for (int lane = 0; lane < 32; ++lane) {
+      const int g = lane >> 2, t = lane & 3;
+      for (int p = 0; p < NPG; ++p)
+        for (int h = 0; h < 2; ++h) o[p * 64 + 2 * lane + h] = op(8 * (2 * p + h) + g, 4 * ks + t);
+      if (lane < 4 * GS) o[NPG * 64 + lane] = op(8 * (NTL - 1) + g, 4 * ks + t);
+    }
+  }
   (void)N;
   return DG_OK;
 }
