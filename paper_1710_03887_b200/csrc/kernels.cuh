@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace dgk {
 
 constexpr int GEO = 25;          // 9 metric terms + 4 faces x (nx, ny, nz, Fscale)
@@ -782,7 +784,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 template <int N>
 struct HO {
   using S = Shape<N>;
-  static constexpr int EB = 8, NW = 16, NT = 32 * NW;
+  static constexpr int EB = 8, NW = 15, CT = 32 * NW, NT = CT + 32;   // + one loader warp
   static constexpr int ROWS = 5 * EB, MT8 = ROWS / 8;
   static constexpr int XS = S::XS;
   static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
@@ -790,6 +792,7 @@ struct HO {
   static constexpr int OPW = NPG * 64 + 4 * GS;                   // doubles per k-step of Op
   static constexpr int KC = (N == 6) ? 6 : 7;                     // k-steps per ring chunk
   static constexpr int NCH = (S::KS4 + KC - 1) / KC;
+  static constexpr int KLAST = S::KS4 - (NCH - 1) * KC;          // k-steps of the last chunk
   static constexpr uint32_t BCH = uint32_t(KC) * OPW * 8;
   static constexpr int MU = (N == 6) ? 3 : 2;                     // 8-row tiles per work item
   static constexpr int SEGW = S::NFP <= 4 ? 4 : S::NFP <= 8 ? 8 : S::NFP <= 16 ? 16 : 32;
@@ -829,13 +832,38 @@ __device__ __forceinline__ HOItem ho_plan(int warp) {
       if ((kind == 0 ? 2 : 1) * mc != wgt) continue;
       int best = -1;
       for (int s = 0; s < 4; ++s)
-        if (cnt[s] < H::NW / 4 && (best < 0 || load[s] < load[best])) best = s;
+        if (s + 4 * cnt[s] < H::NW && (best < 0 || load[s] < load[best])) best = s;
       const int w = best + 4 * cnt[best];
       ++cnt[best];
       load[best] += wgt;
       if (w == warp) mine = HOItem{kind, kind == 0 ? grp : 0, m0, mc};
     }
   return mine;
+}
+
+// KCN k-steps of one ring chunk for a work item of MC row tiles and n-group KIND (0: pair,
+// 1: compacted odd n-tile): one B fragment per k-step, reused MC times
+template <int N, int KIND, int MC, int KCN>
+__device__ __forceinline__ void ho_chunk(double (&acc)[HO<N>::MU][2][2], const double* xa, const double* ob, int kb,
+                                         int lane) {
+  using H = HO<N>;
+#pragma unroll
+  for (int kk = 0; kk < KCN; ++kk) {
+    const int kcol = (kb + kk) * 4;
+    if (KIND == 0) {
+      const double2 b = *reinterpret_cast<const double2*>(ob + kk * H::OPW + 2 * lane);
+#pragma unroll
+      for (int m = 0; m < MC; ++m) {
+        const double a = xa[m * 8 * H::XS + kcol];
+        dmma_8x8x4(acc[m][0], a, b.x);
+        dmma_8x8x4(acc[m][1], a, b.y);
+      }
+    } else {
+      const double b = lane < 4 * H::GS ? ob[kk * H::OPW + lane] : 0.0;
+#pragma unroll
+      for (int m = 0; m < MC; ++m) dmma_8x8x4(acc[m][0], xa[m * 8 * H::XS + kcol], b);
+    }
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -846,7 +874,7 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs A) {
   using S = Shape<N>;
   using H = HO<N>;
-  constexpr int NP = S::NP, NFP = S::NFP, EB = H::EB, NT = H::NT, XS = H::XS, MU = H::MU;
+  constexpr int NP = S::NP, NFP = S::NFP, EB = H::EB, NT = H::NT, CT = H::CT, XS = H::XS, MU = H::MU;
   extern __shared__ __align__(128) unsigned char smem[];
   double* sX = reinterpret_cast<double*>(smem);
   unsigned char* in0 = smem + H::SMEM_X;
@@ -894,10 +922,17 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     mbar_arrive_expect_tx(&sBar[2 + s], bytes);
     tma_load_1d(ring + size_t(s) * (H::BCH / 8), A.op + size_t(c) * H::KC * H::OPW, bytes, &sBar[2 + s]);
   };
-  if (tid == 0 && nmine > 0) {
-    if (is_full(0)) fetch(0);
-    for (long long gc = 0; gc < 2 && gc < nchunks; ++gc) load_chunk(gc);
+  if (warp == H::NW) {
+    // loader warp: keeps the Op ring full, each slot refilled as soon as all compute warps
+    // have released it
+    if (lane == 0)
+      for (long long gn = 0; gn < nchunks; ++gn) {
+        if (gn >= 3) mbar_wait(&sBar[5 + int(gn % 3)], uint32_t(((gn / 3) - 1) & 1));
+        load_chunk(gn);
+      }
+    return;
   }
+  if (tid == 0 && nmine > 0 && is_full(0)) fetch(0);
   const HOItem it = ho_plan<N>(warp);
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
   long long gch = 0;   // chunks consumed so far
@@ -911,18 +946,20 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     double* g_s = bufG(buf);
     int* n_s = bufN(buf);
     uint8_t* c_s = bufC(buf);
+    if (warp == 0) trace_ev(A, j, 0);
     if (tid == 0 && j + 1 < nmine && is_full(j + 1)) fetch(j + 1);   // its buffer was freed by tile j-1
     if (full) {
       mbar_wait(&sBar[buf], (j >> 1) & 1);
     } else {   // the last tile: plain loads, zero-filled
-      for (int i = tid; i < EB * 5 * NP; i += NT) q_s[i] = i < ne * 5 * NP ? __ldg(A.Qin + size_t(e0) * 5 * NP + i) : 0.0;
-      for (int i = tid; i < EB * GEO; i += NT) g_s[i] = i < ne * GEO ? __ldg(A.geo + size_t(e0) * GEO + i) : 0.0;
-      for (int i = tid; i < EB * 4; i += NT) {
+      for (int i = tid; i < EB * 5 * NP; i += CT) q_s[i] = i < ne * 5 * NP ? __ldg(A.Qin + size_t(e0) * 5 * NP + i) : 0.0;
+      for (int i = tid; i < EB * GEO; i += CT) g_s[i] = i < ne * GEO ? __ldg(A.geo + size_t(e0) * GEO + i) : 0.0;
+      for (int i = tid; i < EB * 4; i += CT) {
         n_s[i] = i < ne * 4 ? __ldg(A.nbr + size_t(e0) * 4 + i) : 0;
         c_s[i] = i < ne * 4 ? A.code[size_t(e0) * 4 + i] : uint8_t(CODE_BC + 2);
       }
-      __syncthreads();
+      nbar_sync(1, CT);
     }
+    if (warp == 0) trace_ev(A, j, 1);
     // ---- neighbour traces (one face per SEGW-lane segment, FPASS passes)
     const int seg = lane / H::SEGW, i = lane - seg * H::SEGW;
     const bool lane_ok = i < NFP;
@@ -947,15 +984,17 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         }
       }
     }
+    if (warp == 0) trace_ev(A, j, 2);
     // the previous tile's output bulk stores have left X
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    __syncthreads();
+    nbar_sync(1, CT);
+    if (warp == 0) trace_ev(A, j, 3);
     // ---- volume fluxes -> X[:, 0:3Np)
     if (!(A.debug & 2)) {
-      constexpr int VR = (EB * NP + NT - 1) / NT;
+      constexpr int VR = (EB * NP + CT - 1) / CT;
 #pragma unroll
       for (int rr = 0; rr < VR; ++rr) {
-        const int idx = tid + rr * NT;
+        const int idx = tid + rr * CT;
         if (idx >= ne * NP) break;
         const int e = idx / NP, n = idx - e * NP;
         const double* q = q_s + e * 5 * NP + n;
@@ -979,6 +1018,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         }
       }
     }
+    if (warp == 0) trace_ev(A, j, 4);
     // ---- face terms -> X[:, KVP:KVP+4Nfp)
     if (!(A.debug & 2)) {
       double rip[H::FPASS], unp[H::FPASS], pp[H::FPASS], lam[H::FPASS], unmv[H::FPASS], pmv[H::FPASS];
@@ -1054,59 +1094,60 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
                           row / 5 < ne;
           rprev[m][h][q] = ok ? __ldg(A.res + size_t(e0) * 5 * NP + row * NP + n) : 0.0;
         }
-    __syncthreads();   // X complete
+    if (warp == 0) trace_ev(A, j, 5);
+    nbar_sync(1, CT);   // X complete
+    if (warp == 0) trace_ev(A, j, 6);
     // ---- contraction: Op streams through the ring, chunk by chunk
     double acc[MU][2][2];
 #pragma unroll
     for (int m = 0; m < MU; ++m) acc[m][0][0] = acc[m][0][1] = acc[m][1][0] = acc[m][1][1] = 0.0;
     const double* xa = sX + (it.m0 * 8 + g) * XS + t4;
+#if DG_TRACE
+    long long wfull = 0;
+#endif
     for (int c = 0; c < H::NCH; ++c) {
       const long long gc = gch + c;
       const int s = int(gc % 3);
+#if DG_TRACE
+      long long tw0 = clock64();
+#endif
       mbar_wait(&sBar[2 + s], uint32_t((gc / 3) & 1));
-      const double* ob = ring + size_t(s) * (H::BCH / 8);
-      const int kc = min(H::KC, S::KS4 - c * H::KC);
+#if DG_TRACE
+      wfull += clock64() - tw0;
+#endif
+      const double* ob = ring + size_t(s) * (H::BCH / 8) + (it.kind == 0 ? it.p * 64 : H::NPG * 64);
       if (!(A.debug & 1)) {
-        if (it.kind == 0) {
-#pragma unroll
-          for (int kk = 0; kk < H::KC; ++kk) {
-            if (kk < kc) {
-              const double2 b = *reinterpret_cast<const double2*>(ob + kk * H::OPW + it.p * 64 + 2 * lane);
-              const int kcol = (c * H::KC + kk) * 4;
-#pragma unroll
-              for (int m = 0; m < MU; ++m)
-                if (m < it.mc) {
-                  const double a = xa[m * 8 * XS + kcol];
-                  dmma_8x8x4(acc[m][0], a, b.x);
-                  dmma_8x8x4(acc[m][1], a, b.y);
-                }
-            }
+        // compile-time shape per item and chunk length: unpredicated DMMAs, loads hoisted
+        auto run = [&](auto kcn) {
+          constexpr int KCN = decltype(kcn)::value;
+          const int kb = c * H::KC;
+          if (it.kind == 0) {
+            if (it.mc == 1) ho_chunk<N, 0, 1, KCN>(acc, xa, ob, kb, lane);
+            if (MU >= 2 && it.mc == 2) ho_chunk<N, 0, (MU >= 2 ? 2 : 1), KCN>(acc, xa, ob, kb, lane);
+            if (MU >= 3 && it.mc == 3) ho_chunk<N, 0, (MU >= 3 ? 3 : 1), KCN>(acc, xa, ob, kb, lane);
+          } else if (it.kind == 1) {
+            if (it.mc == 1) ho_chunk<N, 1, 1, KCN>(acc, xa, ob, kb, lane);
+            if (MU >= 2 && it.mc == 2) ho_chunk<N, 1, (MU >= 2 ? 2 : 1), KCN>(acc, xa, ob, kb, lane);
+            if (MU >= 3 && it.mc == 3) ho_chunk<N, 1, (MU >= 3 ? 3 : 1), KCN>(acc, xa, ob, kb, lane);
           }
-        } else if (it.kind == 1) {
-#pragma unroll
-          for (int kk = 0; kk < H::KC; ++kk) {
-            if (kk < kc) {
-              const double b = lane < 4 * H::GS ? ob[kk * H::OPW + H::NPG * 64 + lane] : 0.0;
-              const int kcol = (c * H::KC + kk) * 4;
-#pragma unroll
-              for (int m = 0; m < MU; ++m)
-                if (m < it.mc) dmma_8x8x4(acc[m][0], xa[m * 8 * XS + kcol], b);
-            }
-          }
-        }
+        };
+        if (H::KLAST == H::KC || c + 1 < H::NCH) run(std::integral_constant<int, H::KC>{});
+        else run(std::integral_constant<int, H::KLAST>{});
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sBar[5 + s]);
-      // loader: chunk gc+2 goes into the slot chunk gc-1 used (all warps have released it)
-      if (tid == 0 && gc + 2 < nchunks) {
-        const long long gn = gc + 2;
-        if (gn >= 3) mbar_wait(&sBar[5 + int(gn % 3)], uint32_t(((gn / 3) - 1) & 1));
-        load_chunk(gn);
-      }
       __syncwarp();
     }
     gch += H::NCH;
-    __syncthreads();   // every read of X done: it becomes the output staging tile
+    if (warp == 0) trace_ev(A, j, 7);
+#if DG_TRACE
+    if (tid == 0 && blockIdx.x == 0 && j < 64 && A.trace) {
+      A.trace[j * 16 + 10] = wfull;
+      A.trace[j * 16 + 11] = 0;
+    }
+#endif
+    nbar_sync(1, CT);   // every read of X done: it becomes the output staging tile
+    if (warp == 0) trace_ev(A, j, 8);
     // ---- epilogue
     const bool staged = MODE == MODE_UPDATE && full;
     double* sres = sX;
@@ -1145,7 +1186,8 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         }
       }
     }
-    __syncthreads();   // staging complete; q_s of this tile no longer read
+    if (warp == 0) trace_ev(A, j, 9);
+    nbar_sync(1, CT);   // staging complete; q_s of this tile no longer read
     if (tid == 0 && staged) {
       fence_proxy_async();
       tma_store_1d(A.res + size_t(e0) * 5 * NP, sres, H::BQ);

@@ -25,9 +25,14 @@ assert f(s.ctx, buf, 1024) == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
 names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi", 6: "C eloop", 7: "C barC", 15: "C reswait",
          8: "P start", 9: "P tma", 10: "P XVempty", 11: "P vol", 12: "P fetch", 13: "P XFempty", 14: "P face"}
+if cfg.order >= 5:
+    names = {0: "start", 1: "inputs", 2: "gathers", 3: "Xfree", 4: "vol", 5: "face", 6: "Xsync", 7: "gemm",
+             8: "gsync", 9: "epi"}
 t0 = t[2, 0]
 for j in range(2, 8):
     row = t[j]
+    if cfg.order >= 5:
+        print(f"tile {j}: warp0 full-wait {row[10]} loader empty-wait {row[11]}")
     print(f"tile {j}: " + "  ".join(f"{names[e]}={row[e] - t0}" for e in sorted(names, key=lambda e: row[e])))
 per = (t[10, 0] - t[2, 0]) / 8
 print("cycles per tile (tiles 2..10):", per)
