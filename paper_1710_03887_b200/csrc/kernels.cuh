@@ -225,15 +225,121 @@ struct KBlk {
   static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_;
 };
 
+// Neighbour traces of NPASS face passes (face of pass u: fbase + u fstride; one face per
+// SEGW-lane segment, lane i < NFP its node i): local neighbour / halo record gathers, or the
+// boundary ghost from the own trace; idle lanes keep a finite filler.
+template <int N, int NPASS>
+__device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
+                                            bool lane_ok, const double* q_s, const double* g_s, const int* n_s,
+                                            const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
+                                            const uint8_t* sFm, double (&qp)[NPASS][5]) {
+  constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
+#pragma unroll
+  for (int u = 0; u < NPASS; ++u) {
+    const int face = fbase + u * fstride;
+    const int e = face >> 2, f = face & 3;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
+    if (!(A.debug & 2) && lane_ok && face < flim && e < ne) {
+      const int code = c_s[e * 4 + f];
+      if (code < CODE_BC) {
+        gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
+      } else {   // boundary ghost from the own trace (Q of this tile is in shared memory)
+        const double* G = g_s + e * GEO + 9 + 4 * f;
+        const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
+        double qm[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+        ghost_trace(A, code - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
+      }
+    }
+  }
+}
+
+// Face terms of NPASS passes into the face block of X (row stride XSF, column f Nfp + i):
+// stage 1 both sides' primitives and node speeds (passes as independent chains), stage 2 the
+// face max by an xor butterfly within the SEGW-lane segment (integer pipe: positive doubles
+// order like their bit patterns, idle lanes hold 0), stage 3
+//   Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-)),
+// where the ambient-pressure shift (A14) cancels in n.F(q-) - n.F(q+).  Slots of elements past
+// ne store zeros.
+template <int N, int NPASS, int SEGW, int XSF>
+__device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
+                                           bool lane_ok, const double* q_s, const double* g_s, const uint8_t* sFm,
+                                           const double (&qp)[NPASS][5], double* sXf) {
+  constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
+  if (A.debug & 2) return;
+  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+  double rip[NPASS], unp[NPASS], pp[NPASS], lam[NPASS], unmv[NPASS], pmv[NPASS];
+#pragma unroll
+  for (int u = 0; u < NPASS; ++u) {
+    const int face = fbase + u * fstride;
+    const bool act = lane_ok && face < flim && (face >> 2) < ne;
+    const int fc = act ? face : 0;
+    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+    const double* G = g_s + e * GEO + 9 + 4 * f;
+    const double nx = G[0], ny = G[1], nz = G[2];
+    const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
+    const double qm0 = q[0], qm1 = q[NP], qm2 = q[2 * NP], qm3 = q[3 * NP], qm4 = q[4 * NP];
+    const double rim = rcp_nr(qm0);
+    const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
+    const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
+    unmv[u] = unm;
+    pmv[u] = pm;
+    rip[u] = rcp_nr(qp[u][0]);
+    unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
+    pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
+    const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
+    lam[u] = act ? l : 0.0;
+  }
+  if (A.lambda_mode == 0) {
+#pragma unroll
+    for (int d = 1; d < SEGW; d <<= 1) {
+#pragma unroll
+      for (int u = 0; u < NPASS; ++u) {
+        const long long a = __double_as_longlong(lam[u]);
+        const long long o = __shfl_xor_sync(0xffffffffu, a, d);
+        lam[u] = __longlong_as_double(a > o ? a : o);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NPASS; ++u) {
+    const int face = fbase + u * fstride;
+    const bool slot = lane_ok && face < flim;
+    const bool act = slot && (face >> 2) < ne;
+    const int fc = slot ? face : 0;
+    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+    const double* G = g_s + e * GEO + 9 + 4 * f;
+    const double nx = G[0], ny = G[1], nz = G[2], hfs = act ? 0.5 * G[3] : 0.0;
+    const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
+    double qm[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+    const double pm = pmv[u], unm = unmv[u], dp = pm - pp[u];
+    double df[5];
+    df[0] = fma(qm[0], unm, -qp[u][0] * unp[u]);
+    df[1] = fma(dp, nx, fma(qm[1], unm, -qp[u][1] * unp[u]));
+    df[2] = fma(dp, ny, fma(qm[2], unm, -qp[u][2] * unp[u]));
+    df[3] = fma(dp, nz, fma(qm[3], unm, -qp[u][3] * unp[u]));
+    df[4] = fma(qm[4] + pm, unm, -(qp[u][4] + pp[u]) * unp[u]);
+    double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
+    if (slot) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam[u], qp[u][c] - qm[c], df[c]) : 0.0;
+    }
+  }
+}
+
 template <int N>
 struct WS {
   static constexpr int EB = (N <= 2) ? 32 : 16;
-  // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); 4 consumer warps
-  // keep the DMMA pipes as busy as 8 when the per-element GEMM is small (N = 3, measured on C3)
+  // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 3 the
+  // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3)
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;
 #else
-  static constexpr int PW = 8;
+  static constexpr int PW = N == 3 ? 12 : 8;
 #endif
 #ifdef DG_WS_CW
   static constexpr int CW = DG_WS_CW;
@@ -247,6 +353,7 @@ struct WS {
   // faces per producer warp-pass: one face per power-of-two lane segment (butterfly face max)
   static constexpr int SEGW = Shape<N>::NFP <= 4 ? 4 : Shape<N>::NFP <= 8 ? 8 : Shape<N>::NFP <= 16 ? 16 : 32;
   static constexpr int NSEG = 32 / SEGW;
+  static constexpr int FPASS = (4 * EB + PW * NSEG - 1) / (PW * NSEG);   // face passes per producer warp
   // X is split into its volume block [ROWS][XSV] and face block [ROWS][XSF];
   // strides == 12 (mod 16) doubles keep the A-fragment loads conflict-free
   static constexpr int XSV = (Shape<N>::KVP + 3) / 16 * 16 + 12;
@@ -411,6 +518,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     kloop(KBlk<XSV, 0, S::KSV>{});
     if (io.ctid < 32) trace_ev(A, j, 2);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+
     if (MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // res(j-1) left sRes
       load_res(j);
@@ -548,7 +656,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   if (is_producer) {
     const int ptid = tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
-    const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+    const double gm1 = A.gamma - 1.0;
     auto fetch = [&](int jj) {
       const int tile = blockIdx.x + jj * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
@@ -591,32 +699,12 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ne == EB) mbar_wait(&sBar[buf], (j >> 1) & 1);
       if (ptid < 32) trace_ev(A, j, 9);
       // ---- issue this pwarp's neighbour-trace gathers for the whole tile first: their latency
-      //      hides behind the volume phase (one face per NFP-lane segment, FPASS passes)
+      //      hides behind the volume phase
       const int seg = lane / W::SEGW, i = lane - seg * W::SEGW;
       const bool lane_ok = i < NFP;
-      constexpr int STRIDE = W::PW * W::NSEG;
-      constexpr int FPASS = (EB * 4 + STRIDE - 1) / STRIDE;
-      double qp[FPASS][5];
-#pragma unroll
-      for (int u = 0; u < FPASS; ++u) {
-        const int face = pwarp * W::NSEG + u * STRIDE + seg;
-        const int e = face >> 2, f = face & 3;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];    // finite filler for idle lanes
-        if (!(A.debug & 2) && lane_ok && face < EB * 4 && e < ne) {
-          const int code = c_s[e * 4 + f];
-          if (code < CODE_BC) {
-            gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
-          } else {   // boundary ghost from the own trace (Q of this tile is in shared memory)
-            const double* G = g_s + e * GEO + 9 + 4 * f;
-            const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
-            double qm[5];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
-            ghost_trace(A, code - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
-          }
-        }
-      }
+      const int fbase = pwarp * W::NSEG + seg;
+      double qp[W::FPASS][5];
+      face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       // ---- volume fluxes -> Xv
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       if (ptid < 32) trace_ev(A, j, 10);
@@ -673,76 +761,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ptid < 32) trace_ev(A, j, 12);
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
       if (ptid < 32) trace_ev(A, j, 13);
-      // Stage 1 (all FPASS passes as independent chains): both sides' primitives and node wave
-      // speeds; stage 2: face max; stage 3: fluxes and dF.  The passes interleave, so the FP64
-      // latency of one pass hides behind the others.
-      if (!(A.debug & 2)) {
-        double rip[FPASS], unp[FPASS], pp[FPASS], lam[FPASS], unmv[FPASS], pmv[FPASS];
-        // Stage 1, branch-free: idle lanes work on a clamped (valid) node and are masked below
-#pragma unroll
-        for (int u = 0; u < FPASS; ++u) {
-          const int face = pwarp * W::NSEG + u * STRIDE + seg;
-          const bool act = lane_ok && face < EB * 4 && (face >> 2) < ne;
-          const int fc = act ? face : 0;
-          const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
-          const double* G = g_s + e * GEO + 9 + 4 * f;
-          const double nx = G[0], ny = G[1], nz = G[2];
-          const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
-          const double qm0 = q[0], qm1 = q[NP], qm2 = q[2 * NP], qm3 = q[3 * NP], qm4 = q[4 * NP];
-          const double rim = rcp_nr(qm0);
-          const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
-          const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
-          unmv[u] = unm;
-          pmv[u] = pm;
-          rip[u] = rcp_nr(qp[u][0]);
-          unp[u] = (qp[u][1] * nx + qp[u][2] * ny + qp[u][3] * nz) * rip[u];
-          pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
-          const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
-          lam[u] = act ? l : 0.0;
-        }
-        if (A.lambda_mode == 0) {
-          // face max over the segment's lanes: xor butterfly within the power-of-two segment,
-          // on the integer pipe (positive doubles order like their bit patterns; idle lanes hold 0)
-#pragma unroll
-          for (int d = 1; d < W::SEGW; d <<= 1) {
-#pragma unroll
-            for (int u = 0; u < FPASS; ++u) {
-              const long long a = __double_as_longlong(lam[u]);
-              const long long o = __shfl_xor_sync(0xffffffffu, a, d);
-              lam[u] = __longlong_as_double(a > o ? a : o);
-            }
-          }
-        }
-        // Stage 3, branch-free up to the (predicated) stores
-#pragma unroll
-        for (int u = 0; u < FPASS; ++u) {
-          const int face = pwarp * W::NSEG + u * STRIDE + seg;
-          const bool slot = lane_ok && face < EB * 4;
-          const bool act = slot && (face >> 2) < ne;
-          const int fc = slot ? face : 0;
-          const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
-          const double* G = g_s + e * GEO + 9 + 4 * f;
-          const double nx = G[0], ny = G[1], nz = G[2], hfs = act ? 0.5 * G[3] : 0.0;
-          const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
-          double qm[5];
-#pragma unroll
-          for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
-          const double pm = pmv[u], unm = unmv[u];
-          const double pdm = pm - A.pref, pdp = pp[u] - A.pref;
-          double df[5];
-          df[0] = qm[0] * unm - qp[u][0] * unp[u];
-          df[1] = fma(pdm, nx, qm[1] * unm) - fma(pdp, nx, qp[u][1] * unp[u]);
-          df[2] = fma(pdm, ny, qm[2] * unm) - fma(pdp, ny, qp[u][2] * unp[u]);
-          df[3] = fma(pdm, nz, qm[3] * unm) - fma(pdp, nz, qp[u][3] * unp[u]);
-          df[4] = (qm[4] + pm) * unm - (qp[u][4] + pp[u]) * unp[u];
-          // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-)); zero for idle elements
-          double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
-          if (slot) {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam[u], qp[u][c] - qm[c], df[c]) : 0.0;
-          }
-        }
-      }
+      face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
       if (ptid < 32) trace_ev(A, j, 14);
       nbar_arrive(W::BAR_XF_FULL, NT);
     }
