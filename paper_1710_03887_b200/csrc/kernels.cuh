@@ -486,8 +486,21 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     double acc[NSLOT > 0 ? NSLOT : 1][2];
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u) acc[u][0] = acc[u][1] = 0.0;
+    // the odd n-tile has only GS real columns: with GS <= 4 it is cheaper on DFMA (GS per k-step
+    // and lane, partial sums over the lane's k = t mod 4, reduced by two shuffles) than as a
+    // full 8-column DMMA (16 pipe cycles for GS useful columns)
+    constexpr bool SDF = W::GS > 0 && W::GS <= 4;
+    double sacc[NSING > 0 ? NSING : 1][4];
+#pragma unroll
+    for (int k = 0; k < NSING; ++k) sacc[k][0] = sacc[k][1] = sacc[k][2] = sacc[k][3] = 0.0;
     auto unit_mt = [&](int u) { return u < 2 * NPAIR ? mtp[u >> 1] : mts[u - 2 * NPAIR]; };
     auto unit_nt = [&](int u) { return u < 2 * NPAIR ? ntp[u >> 1] + (u & 1) : S::NTL - 1; };
+    // output column of accumulator (u, q): DMMA fragment layout, or (SDF singles) column t of
+    // the odd n-tile in slot q = 0
+    auto unit_n = [&](int u, int q) {
+      if (SDF && u >= 2 * NPAIR) return q == 0 ? (S::NTL - 1) * 8 + t4 : NP;
+      return unit_nt(u) * 8 + 2 * t4 + q;
+    };
     auto kloop = [&](auto xblk) {
       constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
       if (A.debug & 1) return;
@@ -502,7 +515,17 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           dmma_8x8x4(acc[2 * k], a0, b.x);
           dmma_8x8x4(acc[2 * k + 1], a0, b.y);
         }
-        if (NSING > 0) {
+        if (NSING > 0 && SDF) {
+          double bv[4];
+#pragma unroll
+          for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
+#pragma unroll
+          for (int k = 0; k < NSING; ++k) {
+            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+#pragma unroll
+            for (int c = 0; c < W::GS; ++c) sacc[k][c] = fma(a0, bv[c], sacc[k][c]);
+          }
+        } else if (NSING > 0) {
           const double bs = lane < 4 * W::GS ? ob[W::NPG * 64 + lane] : 0.0;
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
@@ -528,6 +551,20 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     kloop(KBlk<XSF, S::KSV, S::KS4>{});
     if (io.ctid < 32) trace_ev(A, j, 4);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
+    if (SDF) {   // sum the singles' partial products over the 4 lanes of a row; lane t keeps column t
+#pragma unroll
+      for (int k = 0; k < NSING; ++k) {
+        double mine = 0.0;
+#pragma unroll
+        for (int c = 0; c < W::GS; ++c) {
+          double v = sacc[k][c];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (c == t4) mine = v;
+        }
+        acc[2 * NPAIR + k][0] = mine;
+      }
+    }
     const bool staged = MODE == MODE_UPDATE && ne == EB;
     if (staged) mbar_wait(io.barRes, j & 1);   // only the last tile can be partial
     if (io.ctid < 32) trace_ev(A, j, 15);
@@ -542,7 +579,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         for (int u = u0; u < u0 + CH && u < NSLOT; ++u)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const int n = unit_nt(u) * 8 + 2 * t4 + q;
+            const int n = unit_n(u, q);
             const int li = (unit_mt(u) * 8 + g) * NP + (n < NP ? n : 0);
             rv[u - u0][q] = io.sRes[li];
             qv[u - u0][q] = q_s[li];
@@ -551,7 +588,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         for (int u = u0; u < u0 + CH && u < NSLOT; ++u)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const int n = unit_nt(u) * 8 + 2 * t4 + q;
+            const int n = unit_n(u, q);
             if (n >= NP) continue;
             const int li = (unit_mt(u) * 8 + g) * NP + n;   // == (e*5 + c)*NP + n
             const double rr = fma(A.a, rv[u - u0][q], A.dt * acc[u][q]);
@@ -568,7 +605,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         if (e >= ne) continue;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int n = unit_nt(u) * 8 + 2 * t4 + q;
+          const int n = unit_n(u, q);
           if (n >= NP) continue;
           const double rhs = acc[u][q];
           const int li = row * NP + n;
