@@ -40,6 +40,7 @@ extern "C" {
 #endif
 
 #define DG_MAX_ORDER 6
+#define DG_MAX_SENSORS 256
 
 typedef enum dg_status {
   DG_OK = 0,
@@ -167,6 +168,29 @@ dg_status dg_stage_compute(dg_ctx* ctx, int s, double dt, int which, void* strea
 dg_status dg_stage_finish(dg_ctx* ctx, int s, double dt);
 /* same, for one RHS evaluation into `out` (public layout) */
 dg_status dg_rhs_compute(dg_ctx* ctx, double t, double* out, int which, void* stream);
+
+/* ---- point sensors (Table 2: "the generated
+ * pressure was sampled at various positions throughout the computational domain")
+ * dg_sensors_set: n <= DG_MAX_SENSORS points xyz (host, n x 3 row-major, copied).
+ * Each point is located in this rank's elements (barycentric test with tolerance
+ * 1e-10; on a shared face/edge/vertex the element with the smallest global id
+ * wins) and the nodal interpolation weights l_i(r,s,t) of its element are
+ * computed on the host and uploaded.  elem_out (host, n; may be NULL) receives
+ * the public element index on this rank or -1 when the point lies on another
+ * rank or outside the mesh.  Replaces any earlier set; stops recording.
+ * dg_sensors_sample: the state at every sensor -- the conserved variables
+ * interpolated at the point and p = (gamma-1)(E - |m|^2/(2 rho)) from them
+ * (reading A21) -- as n rows (rho, m_x, m_y, m_z, E, p) into out
+ * (device pointer if on_device, else host); rows of sensors not on this rank
+ * are NaN.  Stream-ordered after the stepping calls on the same stream.
+ * dg_sensors_record: from now on every step of dg_rk_step appends one sample
+ * (n x 6 doubles) to the caller's device buffer dbuf (capacity samples; the
+ * caller keeps ownership); NULL stops recording.  dg_sensors_recorded returns
+ * the number of samples written so far. */
+dg_status dg_sensors_set(dg_ctx* ctx, int n, const double* xyz, int32_t* elem_out, void* stream);
+dg_status dg_sensors_sample(dg_ctx* ctx, double* out, int on_device, void* stream);
+dg_status dg_sensors_record(dg_ctx* ctx, double* dbuf, int64_t capacity);
+int64_t dg_sensors_recorded(const dg_ctx* ctx);
 
 /* ---- introspection (tests) ------------------------------------------------ */
 /* Reference operators: r,s,t (Np), Dr/Ds/Dt (Np x Np, row-major), LIFT

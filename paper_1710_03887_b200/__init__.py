@@ -22,6 +22,7 @@ DG_OK, DG_EARG, DG_EMESH, DG_EBLOWUP, DG_ECUDA, DG_ENCCL, DG_EUNSUPPORTED, DG_ES
 DG_BC_INTERIOR, DG_BC_WALL, DG_BC_PASSTHROUGH, DG_BC_INFLOW = 0, 1, 2, 3
 DG_RK_LSERK4, DG_RK_HEUN = 0, 1
 DG_MAX_ORDER = 6
+DG_MAX_SENSORS = 256
 
 SYMBOLS = (
     "dg_mesh_create", "dg_destroy", "dg_last_error", "dg_sizes", "dg_workspace_bytes", "dg_bind_workspace",
@@ -29,6 +30,7 @@ SYMBOLS = (
     "dg_check", "dg_stable_dt", "dg_nccl_get_unique_id", "dg_comm_init", "dg_halo_info", "dg_halo_peer",
     "dg_halo_buffers", "dg_halo_records", "dg_stage_pack", "dg_stage_compute", "dg_stage_finish", "dg_rhs_compute",
     "dg_get_operators", "dg_get_maps", "dg_get_geometry", "dg_launch_count",
+    "dg_sensors_set", "dg_sensors_sample", "dg_sensors_record", "dg_sensors_recorded",
 )
 
 
@@ -96,6 +98,10 @@ def _load():
         "dg_get_maps": (I, [P, pi64, pi64]),
         "dg_get_geometry": (I, [P, pd, pd, pd, pd]),
         "dg_launch_count": (I64, [P]),
+        "dg_sensors_set": (I, [P, I, pd, pi32, P]),
+        "dg_sensors_sample": (I, [P, P, I, P]),
+        "dg_sensors_record": (I, [P, P, I64]),
+        "dg_sensors_recorded": (I64, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -321,6 +327,27 @@ def dg_launch_count(ctx) -> int:
 
 
 # ---------------------------------------------------------------- convenience owner
+def dg_sensors_set(ctx, xyz, stream: int):
+    """Locate n points (n x 3) in this rank's elements; returns the public element index per
+    point (-1: not on this rank)."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    el = np.empty(len(xyz), dtype=np.int32)
+    _check(_lib.dg_sensors_set(ctx, len(xyz), _ptr(xyz, C.c_double), _ptr(el, C.c_int32), stream), ctx)
+    return el
+
+
+def dg_sensors_sample(ctx, out_ptr: int, on_device: bool, stream: int):
+    _check(_lib.dg_sensors_sample(ctx, out_ptr, int(on_device), stream), ctx)
+
+
+def dg_sensors_record(ctx, dbuf_ptr, capacity: int):
+    _check(_lib.dg_sensors_record(ctx, dbuf_ptr, capacity), ctx)
+
+
+def dg_sensors_recorded(ctx) -> int:
+    return int(_lib.dg_sensors_recorded(ctx))
+
+
 class Solver:
     """Owns one ctx and its device workspace (a torch uint8 tensor)."""
 
@@ -382,6 +409,31 @@ class Solver:
 
     def stable_dt(self, cfl: float) -> float:
         return dg_stable_dt(self.ctx, cfl, self.stream)
+
+    # ---- point sensors
+    def set_sensors(self, xyz):
+        """Place sensors at points xyz (n x 3); returns each point's public element (-1: none)."""
+        self._nsens = len(np.asarray(xyz).reshape(-1, 3))
+        self._rec = None
+        return dg_sensors_set(self.ctx, xyz, self.stream)
+
+    def sample_sensors(self):
+        """(n, 6) array: rho, m_x, m_y, m_z, E, p at every sensor (NaN rows: not on this rank)."""
+        out = np.empty((self._nsens, 6), dtype=np.float64)
+        if self._nsens:
+            dg_sensors_sample(self.ctx, out.ctypes.data, False, self.stream)
+        return out
+
+    def record_sensors(self, capacity: int):
+        """Record one sample per RK step into a device buffer of `capacity` samples."""
+        self._rec = self.torch.empty((capacity, self._nsens, 6), dtype=self.torch.float64, device=self.device)
+        dg_sensors_record(self.ctx, self._rec.data_ptr(), capacity)
+
+    def sensor_record(self):
+        """(samples recorded so far, n, 6) array."""
+        n = dg_sensors_recorded(self.ctx)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        return self._rec[:n].cpu().numpy()
 
     @property
     def time(self) -> float:

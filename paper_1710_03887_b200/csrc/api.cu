@@ -132,6 +132,13 @@ cudaError_t launch_pack(dg_ctx* c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_sensors(dg_ctx* c, double* out, cudaStream_t st) {
+  const int threads = 256, grid = (c->nsens * 32 + threads - 1) / threads;
+  dgk::sensor_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], c->dsel, c->dsw, c->nsens, c->Np, c->gamma, out);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
 dgk::StageArgs base_args(dg_ctx* c, double t) {
   dgk::StageArgs A;
   std::memset(&A, 0, sizeof(A));
@@ -257,6 +264,7 @@ size_t dg_workspace_bytes(const dg_ctx* c) {
   const size_t rec = size_t(5) * c->Nfp * 8;
   b += align256(c->nsend * rec) + align256(c->nrecv * rec) + align256(c->nsend * 4) + align256(c->nsend);
   b += align256(64) + align256(4096 * 8);
+  b += align256(size_t(DG_MAX_SENSORS) * c->Np * 8) + align256(size_t(DG_MAX_SENSORS) * 4);   // sensors
   return b;
 }
 
@@ -269,10 +277,12 @@ dg_status dg_memory_report(const dg_ctx* c, size_t bytes[7]) {
   bytes[2] = st;
   bytes[3] = size_t(c->K) * dgk::GEO * 8;
   bytes[4] = size_t(c->K) * (16 + 4 + 4 + 8);
-  bytes[5] = c->opfrag.size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp;
+  bytes[5] = c->opfrag.size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp + size_t(DG_MAX_SENSORS) * (c->Np * 8 + 4);
   bytes[6] = (c->nsend + c->nrecv) * rec + c->nsend * 5;
   return DG_OK;
 }
+
+static dg_status upload_sensors(dg_ctx* c, cudaStream_t st);
 
 dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) {
   if (!c || !dptr) return set_err(c, DG_EARG, "NULL argument");
@@ -304,6 +314,9 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   c->dsface = reinterpret_cast<uint8_t*>(take(c->nsend));
   c->dflag = reinterpret_cast<int*>(take(64));
   c->dscratch = reinterpret_cast<double*>(take(4096 * 8));
+  c->dsw = reinterpret_cast<double*>(take(size_t(DG_MAX_SENSORS) * c->Np * 8));
+  c->dsel = reinterpret_cast<int32_t*>(take(size_t(DG_MAX_SENSORS) * 4));
+  c->rec_buf = nullptr;
   c->ws = dptr;
   c->ws_bytes = nbytes;
   dg_memory_report(c, c->cat_bytes);
@@ -324,6 +337,10 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   }
   CUDA_TRY(c, cudaMemsetAsync(c->dflag, 0, 64, st));
   CUDA_TRY(c, cudaMemsetAsync(c->dQ[0], 0, 3 * align256(stb), st));
+  if (c->nsens > 0) {   // sensors placed before the workspace was bound
+    dg_status e = upload_sensors(c, st);
+    if (e) return e;
+  }
   CUDA_TRY(c, cudaStreamSynchronize(st));   // host vectors above are pageable / temporaries
   return DG_OK;
 }
@@ -478,6 +495,10 @@ dg_status dg_rk_step(dg_ctx* c, double dt, int nsteps, void* stream) {
         if (e) return e;
       }
       dg_stage_finish(c, s, dt);
+    }
+    if (c->rec_buf && c->nsens > 0 && c->rec_count < c->rec_cap) {
+      CUDA_TRY(c, launch_sensors(c, c->rec_buf + c->rec_count * c->nsens * 6, st));
+      ++c->rec_count;
     }
     if (c->check_every > 0 && (c->steps_done % c->check_every) == 0) {
       dg_status e = dg_check(c, stream);
@@ -636,6 +657,109 @@ dg_status dg_get_geometry(const dg_ctx* c, double* J, double* rx9, double* n12, 
 }
 
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+static dg_status upload_sensors(dg_ctx* c, cudaStream_t st) {
+  if (c->nsens == 0 || !c->ws) return DG_OK;
+  CUDA_TRY(c, cudaMemcpyAsync(c->dsw, c->sens_w.data(), c->sens_w.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dsel, c->sens_elem.data(), size_t(c->nsens) * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));   // the host vectors may change on the next call
+  return DG_OK;
+}
+
+dg_status dg_sensors_set(dg_ctx* c, int n, const double* xyz, int32_t* elem_out, void* stream) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  if (n < 0 || n > DG_MAX_SENSORS || (n > 0 && !xyz)) return set_err(c, DG_EARG, "sensor count out of range or NULL points");
+  const int Np = c->Np;
+  const int64_t K = c->K;
+  // reference corner nodes (v1..v4) of the node set
+  int corner[4] = {-1, -1, -1, -1};
+  const double cr[4][3] = {{-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {-1, -1, 1}};
+  for (int v = 0; v < 4; ++v)
+    for (int q = 0; q < Np; ++q)
+      if (std::fabs(c->ref.r[q] - cr[v][0]) < 1e-12 && std::fabs(c->ref.s[q] - cr[v][1]) < 1e-12 &&
+          std::fabs(c->ref.t[q] - cr[v][2]) < 1e-12)
+        corner[v] = q;
+  for (int v = 0; v < 4; ++v)
+    if (corner[v] < 0) return set_err(c, DG_EARG, "reference corner node not found");
+  std::vector<int32_t> el(n, -1);
+  std::vector<int64_t> best_gid(n, INT64_MAX);
+  std::vector<double> rst(3 * size_t(n), 0.0);
+  const double tol = 1e-10;
+  const size_t KN = size_t(K) * Np;
+  for (int64_t l = 0; l < K; ++l) {
+    const int64_t pb = c->pub[l];
+    double vx[4][3];
+    for (int v = 0; v < 4; ++v)
+      for (int d = 0; d < 3; ++d) vx[v][d] = c->xyz[d * KN + size_t(pb) * Np + corner[v]];
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(std::min(vx[0][d], vx[1][d]), std::min(vx[2][d], vx[3][d]));
+      hi[d] = std::max(std::max(vx[0][d], vx[1][d]), std::max(vx[2][d], vx[3][d]));
+    }
+    const double pad = 1e-9 * (hi[0] - lo[0] + hi[1] - lo[1] + hi[2] - lo[2]);
+    const double* G = &c->geo[size_t(l) * 25];
+    for (int i = 0; i < n; ++i) {
+      const double* x = xyz + 3 * size_t(i);
+      if (x[0] < lo[0] - pad || x[0] > hi[0] + pad || x[1] < lo[1] - pad || x[1] > hi[1] + pad ||
+          x[2] < lo[2] - pad || x[2] > hi[2] + pad)
+        continue;
+      const double d0 = x[0] - vx[0][0], d1 = x[1] - vx[0][1], d2 = x[2] - vx[0][2];
+      // (1+r, 1+s, 1+t) = (grad r, grad s, grad t) . (x - v1)
+      const double r1 = G[0] * d0 + G[1] * d1 + G[2] * d2;
+      const double s1 = G[3] * d0 + G[4] * d1 + G[5] * d2;
+      const double t1 = G[6] * d0 + G[7] * d1 + G[8] * d2;
+      const double lam[4] = {1.0 - (r1 + s1 + t1) / 2, r1 / 2, s1 / 2, t1 / 2};   // barycentrics of v1..v4
+      if (lam[0] < -tol || lam[1] < -tol || lam[2] < -tol || lam[3] < -tol) continue;
+      if (c->gid[l] < best_gid[i]) {
+        best_gid[i] = c->gid[l];
+        el[i] = int32_t(l);
+        rst[3 * i] = r1 - 1.0;
+        rst[3 * i + 1] = s1 - 1.0;
+        rst[3 * i + 2] = t1 - 1.0;
+      }
+    }
+  }
+  c->nsens = n;
+  c->sens_elem = el;
+  c->sens_w.assign(size_t(n) * Np, 0.0);
+  for (int i = 0; i < n; ++i) {
+    if (el[i] >= 0) dgb::interp_weights(c->ref, rst[3 * i], rst[3 * i + 1], rst[3 * i + 2], &c->sens_w[size_t(i) * Np]);
+    if (elem_out) elem_out[i] = el[i] >= 0 ? c->pub[el[i]] : -1;
+  }
+  dg_status e = upload_sensors(c, static_cast<cudaStream_t>(stream));   // or at dg_bind_workspace
+  if (e) return e;
+  c->rec_buf = nullptr;
+  c->rec_cap = c->rec_count = 0;
+  return DG_OK;
+}
+
+dg_status dg_sensors_sample(dg_ctx* c, double* out, int on_device, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!out) return set_err(c, DG_EARG, "NULL output");
+  if (!c->state_set) return set_err(c, DG_ESTATE, "state not set");
+  if (c->nsens == 0) return DG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* dst = on_device ? out : c->dscratch;   // scratch holds 4096 doubles >= 256 x 6
+  CUDA_TRY(c, launch_sensors(c, dst, st));
+  if (!on_device) {
+    CUDA_TRY(c, cudaMemcpyAsync(out, dst, size_t(c->nsens) * 6 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+  }
+  return DG_OK;
+}
+
+dg_status dg_sensors_record(dg_ctx* c, double* dbuf, int64_t capacity) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (dbuf && capacity <= 0) return set_err(c, DG_EARG, "capacity must be positive");
+  c->rec_buf = dbuf;
+  c->rec_cap = dbuf ? capacity : 0;
+  c->rec_count = 0;
+  return DG_OK;
+}
+
+int64_t dg_sensors_recorded(const dg_ctx* c) { return c ? c->rec_count : 0; }
 
 // Debug only (DG_TRACE builds): copy the phase-timestamp scratch of the last stage launch.
 dg_status dg_debug_trace(const dg_ctx* c, unsigned long long* out, int n) {

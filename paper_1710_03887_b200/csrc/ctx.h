@@ -64,6 +64,15 @@ struct dg_ctx {
   double* dscratch = nullptr;
   size_t cat_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
 
+  // ---- point sensors
+  int nsens = 0;
+  std::vector<int32_t> sens_elem;   // internal element or -1 (not on this rank)
+  std::vector<double> sens_w;       // nsens x Np interpolation weights
+  double* dsw = nullptr;            // device: DG_MAX_SENSORS x Np weights
+  int32_t* dsel = nullptr;          // device: DG_MAX_SENSORS elements
+  double* rec_buf = nullptr;        // caller's device buffer, rec_cap x nsens x 6
+  int64_t rec_cap = 0, rec_count = 0;
+
   // ---- run state
   int cur = 0;          // which dQ holds the current state
   double t = 0.0;

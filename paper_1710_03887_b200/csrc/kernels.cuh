@@ -1315,4 +1315,34 @@ __global__ void max_speed_kernel(const double* __restrict__ Q, int64_t nnode, in
   }
 }
 
+// point sensors: one warp per sensor interpolates the five conserved
+// variables with the host-computed nodal weights, then forms p from them; NaN rows for
+// sensors that are not on this rank
+__global__ void sensor_kernel(const double* __restrict__ Q, const int32_t* __restrict__ el,
+                              const double* __restrict__ w, int n, int Np, double gamma, double* __restrict__ out) {
+  const int sid = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (sid >= n) return;
+  double* o = out + size_t(sid) * 6;
+  const int k = el[sid];
+  if (k < 0) {
+    if (lane < 6) o[lane] = __longlong_as_double(0x7ff8000000000000LL);
+    return;
+  }
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int j = lane; j < Np; j += 32) {
+    const double wj = w[size_t(sid) * Np + j];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) acc[c] = fma(wj, Q[(size_t(k) * 5 + c) * Np + j], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < 5; ++c)
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], d);
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) o[c] = acc[c];
+    o[5] = (gamma - 1.0) * (acc[4] - 0.5 * (acc[1] * acc[1] + acc[2] * acc[2] + acc[3] * acc[3]) / acc[0]);
+  }
+}
+
 }  // namespace dgk

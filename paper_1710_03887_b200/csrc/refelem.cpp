@@ -307,6 +307,7 @@ bool build_reference(int N, RefElem& R, std::string* msg) {
           pkdo3(R.r[n], R.s[n], R.t[n], i, j, k, V[n * Np + m], Vr[n * Np + m], Vs[n * Np + m], Vt[n * Np + m]);
   std::vector<double> Vinv = V;
   if (!invert(Vinv, Np)) { if (msg) *msg = "singular Vandermonde"; return false; }
+  R.Vinv = Vinv;
   R.Dr = matmul(Vr, Vinv, Np, Np, Np);
   R.Ds = matmul(Vs, Vinv, Np, Np, Np);
   R.Dt = matmul(Vt, Vinv, Np, Np, Np);
@@ -346,6 +347,23 @@ bool build_reference(int N, RefElem& R, std::string* msg) {
     }
   R.LIFT = matmul(VVt, E, Np, Np, 4 * Nfp);
   return true;
+}
+
+void interp_weights(const RefElem& R, double r, double s, double t, double* w) {
+  const int N = R.N, Np = R.Np;
+  std::vector<double> psi(Np);
+  int m = 0;
+  for (int i = 0; i <= N; ++i)
+    for (int j = 0; j <= N - i; ++j)
+      for (int k = 0; k <= N - i - j; ++k, ++m) {
+        double dr, ds, dt;
+        pkdo3(r, s, t, i, j, k, psi[m], dr, ds, dt);
+      }
+  for (int n = 0; n < Np; ++n) {
+    double acc = 0;
+    for (int j = 0; j < Np; ++j) acc += R.Vinv[j * Np + n] * psi[j];
+    w[n] = acc;
+  }
 }
 
 }  // namespace dgb

@@ -23,6 +23,7 @@ struct RefElem {
   // face f2 of my face node i when my face vertex m matches neighbour face
   // vertex PERM[sigma][m]
   std::vector<int> nbr_local;
+  std::vector<double> Vinv;             // Np x Np inverse Vandermonde (orthonormal basis)
 };
 
 extern const int FACE_VERTS[4][3];
@@ -33,5 +34,8 @@ inline int n_face_nodes(int N) { return (N + 1) * (N + 2) / 2; }
 
 // Builds everything above; returns false (with msg) on numerical failure.
 bool build_reference(int N, RefElem& R, std::string* msg);
+
+// Nodal interpolation weights at a reference point: w_i = l_i(r,s,t) = sum_j Vinv[j][i] psi_j(r,s,t).
+void interp_weights(const RefElem& R, double r, double s, double t, double* w);
 
 }  // namespace dgb
