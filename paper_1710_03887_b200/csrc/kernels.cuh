@@ -375,14 +375,19 @@ struct WS {
   static constexpr size_t SMEM_XV = size_t(ROWS) * XSV * 8;
   static constexpr size_t SMEM_XF = size_t(ROWS) * XSF * 8;
   static constexpr size_t SMEM_OP = (size_t(OPC) * 8 + 15) / 16 * 16;
-  static constexpr size_t SMEM_IN = size_t(2) * BIN;
-  static constexpr size_t SMEM_RES = BQ;                                  // residual tile (TMA in/out)
+  // input buffers (Q, geometry, connectivity) and residual tiles: 3 and 2 when they fit (the
+  // producers then never wait for the consumers' epilogue, the residual arrives a tile early),
+  // else 2 and 1
   static constexpr size_t SMEM_T = size_t(2 * 96 * Shape<N>::NFP + 4 * Shape<N>::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_RES + SMEM_T + 32;
+  static constexpr bool DEEP = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_T + 64 + 3 * size_t(BIN) + 2 * size_t(BQ) <= 227 * 1024;
+  static constexpr int NIN = DEEP ? 3 : 2, NRES = DEEP ? 2 : 1;
+  static constexpr size_t SMEM_IN = size_t(NIN) * BIN;
+  static constexpr size_t SMEM_RES = size_t(NRES) * BQ;                  // residual tiles (TMA in/out)
+  static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_RES + SMEM_T + 64;
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
   static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
-                       BAR_Q_EMPTY = 6 /* and 7 */, BAR_C = 8;
+                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9;
 };
 
 #ifndef DG_KUNROLL
@@ -470,19 +475,21 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
     return A.e_end - e0 >= EB;
   };
-  auto load_res = [&](int jj) {   // one thread; the previous bulk store has finished reading sRes
+  auto res_buf = [&](int jj) { return io.sRes + (jj % W::NRES) * (W::BQ / 8); };
+  auto load_res = [&](int jj) {   // one thread; the last bulk store from that buffer has been read
     const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
     fence_proxy_async();
-    mbar_arrive_expect_tx(io.barRes, W::BQ);
-    tma_load_1d(io.sRes, A.res + size_t(e0) * 5 * NP, W::BQ, io.barRes);
+    mbar_arrive_expect_tx(io.barRes + jj % W::NRES, W::BQ);
+    tma_load_1d(res_buf(jj), A.res + size_t(e0) * 5 * NP, W::BQ, io.barRes + jj % W::NRES);
   };
   if (MODE == MODE_UPDATE && io.ctid == 0 && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     const int e0 = A.e_begin + tile * EB;
     const int ne = min(EB, A.e_end - e0);
-    const int buf = j & 1;
+    const int buf = j % W::NIN;
     double* q_s = reinterpret_cast<double*>(io.in0 + buf * W::BIN);
+    double* sRes = res_buf(j);
     double acc[NSLOT > 0 ? NSLOT : 1][2];
 #pragma unroll
     for (int u = 0; u < NSLOT; ++u) acc[u][0] = acc[u][1] = 0.0;
@@ -542,7 +549,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 2);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
 
-    if (MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
+    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // res(j-1) left sRes
       load_res(j);
     }
@@ -566,7 +573,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       }
     }
     const bool staged = MODE == MODE_UPDATE && ne == EB;
-    if (staged) mbar_wait(io.barRes, j & 1);   // only the last tile can be partial
+    if (staged) mbar_wait(io.barRes + j % W::NRES, (j / W::NRES) & 1);   // only the last tile can be partial
     if (io.ctid < 32) trace_ev(A, j, 15);
     if (staged) {
       // in chunks of CH units: all loads of a chunk first (q_s and sRes could alias as far as the
@@ -581,7 +588,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           for (int q = 0; q < 2; ++q) {
             const int n = unit_n(u, q);
             const int li = (unit_mt(u) * 8 + g) * NP + (n < NP ? n : 0);
-            rv[u - u0][q] = io.sRes[li];
+            rv[u - u0][q] = sRes[li];
             qv[u - u0][q] = q_s[li];
           }
 #pragma unroll
@@ -593,7 +600,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             const int li = (unit_mt(u) * 8 + g) * NP + n;   // == (e*5 + c)*NP + n
             const double rr = fma(A.a, rv[u - u0][q], A.dt * acc[u][q]);
             const double qn = fma(A.b, rr, qv[u - u0][q]);
-            io.sRes[li] = rr;
+            sRes[li] = rr;
             q_s[li] = qn;
           }
       }
@@ -630,15 +637,18 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         fence_proxy_async();
         tma_store_1d(A.Qout + size_t(e0) * 5 * NP, q_s, W::BQ);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        tma_store_1d(A.res + size_t(e0) * 5 * NP, io.sRes, W::BQ);
+        tma_store_1d(A.res + size_t(e0) * 5 * NP, sRes, W::BQ);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        // two residual buffers: the next tile's goes where tile j-1's was stored from (that
+        // store is older than the Q store just waited for)
+        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) load_res(j + 1);
       }
     }
     if (io.ctid < 32) trace_ev(A, j, 5);
     // only consumer warp 0 signals the Q buffer free (after BAR_C and its lane 0 saw the Q
     // bulk read finish)
-    if (j + 2 < io.nmine && io.ctid < 32) {
+    if (j + W::NIN < io.nmine && io.ctid < 32) {
       __syncwarp();
       nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
     }
@@ -662,11 +672,11 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * W::BIN + W::BQ); };
   auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * W::BIN + W::BQ + W::BG); };
   auto bufC = [&](int b) { return reinterpret_cast<uint8_t*>(in0 + b * W::BIN + W::BQ + W::BG + W::BN); };
-  double* sRes = reinterpret_cast<double*>(in0 + 2 * W::BIN);
-  uint8_t* sTbl = reinterpret_cast<uint8_t*>(in0 + 2 * W::BIN + W::SMEM_RES);
+  double* sRes = reinterpret_cast<double*>(in0 + W::SMEM_IN);
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(in0 + W::SMEM_IN + W::SMEM_RES);
   uint8_t* sTblf = sTbl + 96 * NFP;
   uint8_t* sFm = sTblf + 96 * NFP;
-  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);   // [0,1] inputs, [2] residual
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);   // NIN inputs, then NRES residuals
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // B operand (mesh.cpp layout: per k-step the n-tile pairs, then the compacted odd n-tile)
@@ -678,9 +688,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
   for (int i = tid; i < W::ROWS * (XSV + XSF); i += NT) sXv[i] = 0.0;   // padding columns stay 0
   if (tid == 0) {
-    mbar_init(&sBar[0], 1);
-    mbar_init(&sBar[1], 1);
-    mbar_init(&sBar[2], 1);
+    for (int b = 0; b < W::NIN + W::NRES; ++b) mbar_init(&sBar[b], 1);   // inputs, then residuals
   }
   __syncthreads();
 
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int tile = blockIdx.x + jj * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
       const int ne = min(EB, A.e_end - e0);
-      const int b = jj & 1;
+      const int b = jj % W::NIN;
       if (ne == EB) {
         if (ptid == 0) {
           fence_proxy_async();
@@ -727,13 +735,13 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int tile = blockIdx.x + j * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
       const int ne = min(EB, A.e_end - e0);
-      const int buf = j & 1;
+      const int buf = j % W::NIN;
       const double* q_s = bufQ(buf);
       const double* g_s = bufG(buf);
       const int* n_s = bufN(buf);
       const uint8_t* c_s = bufC(buf);
       if (ptid < 32) trace_ev(A, j, 8);
-      if (ne == EB) mbar_wait(&sBar[buf], (j >> 1) & 1);
+      if (ne == EB) mbar_wait(&sBar[buf], (j / W::NIN) & 1);
       if (ptid < 32) trace_ev(A, j, 9);
       // ---- issue this pwarp's neighbour-trace gathers for the whole tile first: their latency
       //      hides behind the volume phase
@@ -791,7 +799,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1;
       //      the Q_EMPTY sync also covers every producer thread having left tile j-1)
       if (j + 1 < nmine) {
-        if (j + 1 >= 2) nbar_sync(W::BAR_Q_EMPTY + ((j + 1) & 1), W::PT + 32);
+        if (j + 1 >= W::NIN) nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
         fetch(j + 1);
       }
       // ---- face fluxes -> Xf
@@ -808,7 +816,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     // without run-time branches
     using PL = M8Plan<N>;
     const int cw = warp;
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[2], nmine, tid, lane};
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], nmine, tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
