@@ -74,3 +74,24 @@ def test_sensor_recording_matches_sampling():
     s.step(dt, 3)                                         # capacity 4: one more sample, then full
     assert dg.dg_sensors_recorded(s.ctx) == 4
     s.close()
+
+
+def test_recorded_pressure_spectrum_on_device():
+    """N4 pipeline on a device record: torch.fft on the GPU vs the oracle's DFT sums."""
+    from oracle import analysis as oan
+    from paper_1710_03887_b200 import analysis as pan
+    cfg = configs.make("C2", scale=0.25)
+    s = _solver(cfg)
+    s.set_state(configs.initial_state(cfg, s.nodes()))
+    dt = s.stable_dt(0.5)
+    s.set_sensors(_points(cfg, 3, 4))
+    s.record_sensors(16)
+    s.step(dt, 16)
+    torch.cuda.synchronize()
+    p = s._rec[:, :, 5]                          # (16, 3) pressure, on the device
+    f, db, a = pan.spectrum(p, dt)
+    assert a.is_cuda
+    for i in range(3):
+        f0, db0, a0 = oan.dft_amplitude(p[:, i].cpu().numpy(), dt)
+        assert np.abs(a[:, i].cpu().numpy() - a0).max() < 1e-15 + 1e-12 * a0.max()
+    s.close()
