@@ -21,6 +21,7 @@ euler    pressure, Euler fluxes (Eq. 1-2), ghosts (Eq. 3-4, 5-7), LLF flux (P:41
 rhs      strong-form nodal DG right-hand side f(Q, t)
 timestep LSERK4 (Carpenter-Kennedy) and Heun RK2 in 2N-storage form
 sensors  point location and nodal evaluation at sensor points       (Table 2)
+modal    the paper's modal scheme: orthonormal basis, Gauss rules, weak-form RHS (N3)
 analysis DFT amplitude spectra, decay exponent, percent of atmosphere
 
 Parity status: every function is pinned by ``tests/test_oracle_*.py`` except
