@@ -45,6 +45,16 @@ def flops_per_elem_stage(N: int) -> float:
     return 30 * Np ** 2 + 40 * Np * Nfp + 110 * Np + 480 * Nfp + 25 * Np
 
 
+def flops_per_elem_stage_modal(p: int) -> float:
+    """Algorithmic FLOPs per element per stage of the modal-quadrature scheme (A23):
+    interpolation to NQ = (p+1)^3 volume and 4 NQF = 4 (p+1)^2 face points (own and neighbour),
+    fluxes there, weak-form projections back onto Np modes, the update."""
+    Np = (p + 1) * (p + 2) * (p + 3) // 6
+    NQ, NQF = (p + 1) ** 3, (p + 1) ** 2
+    return (2 * NQ * Np * 5 + 110 * NQ + 2 * 3 * NQ * Np * 5          # volume
+            + 2 * 2 * 4 * NQF * Np * 5 + 120 * 4 * NQF + 2 * 4 * NQF * Np * 5 + 25 * Np)   # faces, update
+
+
 def bytes_per_elem_stage(N: int) -> float:
     """Compulsory HBM bytes per element per stage: Q and res read+written + geometry + connectivity."""
     Np = (N + 1) * (N + 2) * (N + 3) // 6
@@ -125,10 +135,14 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = build_config(args.config, world)
+    if args.order:
+        cfg.order = args.order
+    modal = args.scheme == "modal"
     m = cfg.mesh
     part = smesh.x_slab_partition(m, world) if world > 1 else None
     s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma, q_inf=cfg.q_inf,
-                  part=part, nparts=world, rank=rank)
+                  part=part, nparts=world, rank=rank,
+                  scheme=dg.DG_SCHEME_MODAL if modal else dg.DG_SCHEME_NODAL)
     if world > 1:
         uid = [dg.dg_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -176,11 +190,12 @@ def run_ours(args):
     if world > 1 and per_launch_ms is not None:
         per_launch_ms = ms / (STAGES * args.steps)
     K_loc = s.K
-    flops_launch = flops_per_elem_stage(cfg.order) * K_loc
+    fpe = flops_per_elem_stage_modal(cfg.order) if modal else flops_per_elem_stage(cfg.order)
+    flops_launch = fpe * K_loc
     achieved = flops_launch / (per_launch_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_summary_{args.config}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and not modal and not args.order:
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
@@ -211,13 +226,13 @@ def run_ours(args):
     state_bytes = 5 * K_loc * s.Np * 8
 
     if rank == 0:
-        cpu = cpu_baseline(args, cfg) if (world == 1 and not args.no_cpu_baseline) else None
+        cpu = cpu_baseline(args, cfg) if (world == 1 and not args.no_cpu_baseline and not modal) else None
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
             "scaling": "weak" if args.config == "C5" else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded mesh + isentropic Gaussian pulse, DESIGN.md input recipe)",
-            "config": {"workload": f"{args.config}: K={K_tot} affine tets, N={cfg.order}, Np={s.Np}, "
+            "config": {"workload": f"{args.config}{' modal-quadrature scheme' if modal else ''}: K={K_tot} affine tets, N={cfg.order}, Np={s.Np}, "
                                    f"{len(cfg.pulses)} pulse(s), LSERK4 dt={dt:.4g} (CFL {cfg.cfl})",
                        "elements": K_tot, "order": cfg.order, "dofs": dofs, "stages_per_step": STAGES,
                        "parallelism": f"x-slab element partition x{world}" if world > 1 else "single GPU",
@@ -225,7 +240,7 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
                          "peak_source": "measured FP64 DMMA (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64",
-                         "flops_per_elem_stage": flops_per_elem_stage(cfg.order),
+                         "flops_per_elem_stage": fpe,
                          "hbm_bytes_per_elem_stage": bytes_per_elem_stage(cfg.order),
                          "hbm_frac": round(bytes_per_elem_stage(cfg.order) * K_loc / (per_launch_ms * 1e-3) / 1e9
                                            / measured_peaks().get("hbm_gbs", 6545.0), 4)},
@@ -330,6 +345,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scheme", default="nodal", choices=["nodal", "modal"],
+                    help="modal = the paper's modal-quadrature scheme (orders 1-3; SURVEY N3)")
+    ap.add_argument("--order", type=int, default=0, help="override the config's polynomial order")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)

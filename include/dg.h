@@ -60,6 +60,10 @@ enum { DG_BC_INTERIOR = 0, DG_BC_WALL = 1, DG_BC_PASSTHROUGH = 2, DG_BC_INFLOW =
 /* time integrators ("RK2"; BASELINE.json configs: LSERK4) */
 enum { DG_RK_LSERK4 = 0, DG_RK_HEUN = 1 };
 
+/* spatial schemes: nodal collocation (default) or the paper's own modal
+ * scheme with Gauss quadrature (orders 1-3, one partition) */
+enum { DG_SCHEME_NODAL = 0, DG_SCHEME_MODAL = 1 };
+
 typedef struct dg_ctx dg_ctx;
 
 typedef struct dg_mesh_desc {
@@ -82,6 +86,10 @@ typedef struct dg_mesh_desc {
   int check_every;           /* dg_rk_step checks the blow-up flag every n steps (0 = never) */
   int rk_scheme;             /* DG_RK_LSERK4 (default) or DG_RK_HEUN                         */
   double inflow_alpha;       /* pulse angular frequency of the inflow BC, 565   */
+  int scheme;                /* DG_SCHEME_NODAL (default) or DG_SCHEME_MODAL: the state of   */
+                             /* dg_set_state / dg_get_state / dg_rhs stays nodal values at   */
+                             /* the dg_get_nodes points; internally the modal scheme steps   */
+                             /* orthonormal coefficients (interpolation c = V^-1 u, A23)     */
 } dg_mesh_desc;
 
 /* Build a context for `rank` (0 <= rank < nparts): validate the mesh, fix or

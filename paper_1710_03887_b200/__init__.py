@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libdg_b200.so")
 DG_OK, DG_EARG, DG_EMESH, DG_EBLOWUP, DG_ECUDA, DG_ENCCL, DG_EUNSUPPORTED, DG_ESTATE = 0, 2, 3, 4, 5, 6, 7, 8
 DG_BC_INTERIOR, DG_BC_WALL, DG_BC_PASSTHROUGH, DG_BC_INFLOW = 0, 1, 2, 3
 DG_RK_LSERK4, DG_RK_HEUN = 0, 1
+DG_SCHEME_NODAL, DG_SCHEME_MODAL = 0, 1
 DG_MAX_ORDER = 6
 DG_MAX_SENSORS = 256
 
@@ -58,6 +59,7 @@ class dg_mesh_desc(C.Structure):
         ("check_every", C.c_int),
         ("rk_scheme", C.c_int),
         ("inflow_alpha", C.c_double),
+        ("scheme", C.c_int),
     ]
 
 
@@ -143,7 +145,7 @@ def _check(status, ctx=None):
 # ---------------------------------------------------------------- C-named wrappers
 def dg_mesh_create(order, vxyz, etov, bc, *, etoe=None, etof=None, gamma=1.4, q_inf=(1.4, 0, 0, 0, 2.5),
                    part=None, nparts=1, rank=0, lambda_mode=0, check_every=0, rk_scheme=DG_RK_LSERK4,
-                   inflow_alpha=565.0):
+                   inflow_alpha=565.0, scheme=DG_SCHEME_NODAL):
     """Returns an opaque ctx handle (int).  Host arrays are copied by the library."""
     vxyz = np.ascontiguousarray(vxyz, dtype=np.float64)
     etov = np.ascontiguousarray(etov, dtype=np.int64)
@@ -169,6 +171,7 @@ def dg_mesh_create(order, vxyz, etov, bc, *, etoe=None, etof=None, gamma=1.4, q_
     d.check_every = int(check_every)
     d.rk_scheme = int(rk_scheme)
     d.inflow_alpha = float(inflow_alpha)
+    d.scheme = int(scheme)
     out = C.c_void_p()
     _check(_lib.dg_mesh_create(C.byref(d), int(rank), C.byref(out)))
     return out.value

@@ -132,6 +132,47 @@ cudaError_t launch_pack(dg_ctx* c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// operator tables uploaded to the workspace: DMMA B fragments (nodal) or the modal tables
+const std::vector<double>& op_host(const dg_ctx* c) { return c->scheme == DG_SCHEME_MODAL ? c->modal_cat : c->opfrag; }
+
+template <int P, int MODE>
+cudaError_t launch_modal_p(const dgk::StageArgs& A, cudaStream_t st) {
+  using M = dgk::MS<P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgk::modal_stage_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(M::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ntiles = (A.e_end - A.e_begin + M::EB - 1) / M::EB;
+  if (ntiles <= 0) return cudaSuccess;
+  dgk::modal_stage_kernel<P, MODE><<<ntiles, M::NT, M::SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_modal(int P, const dgk::StageArgs& A, cudaStream_t st) {
+  switch (P) {
+    case 1: return launch_modal_p<1, MODE>(A, st);
+    case 2: return launch_modal_p<2, MODE>(A, st);
+    case 3: return launch_modal_p<3, MODE>(A, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// per element and field: out = Mat in (Mat = V^-1: nodal -> modal; V: modal -> nodal)
+cudaError_t modal_convert(dg_ctx* c, const double* in, double* out, bool to_modal, cudaStream_t st) {
+  const int64_t n = c->K * 5 * c->Np;
+  const int threads = 256;
+  const int P = c->N;
+  const size_t off = to_modal ? size_t(c->modal_cat.size() - size_t(c->Np) * c->Np)
+                              : size_t(c->modal_cat.size() - 2 * size_t(c->Np) * c->Np);
+  (void)P;
+  dgk::modal_convert_kernel<<<int((n + threads - 1) / threads), threads, 0, st>>>(in, out, c->dop + off, c->K, c->Np);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sensors(dg_ctx* c, double* out, cudaStream_t st) {
   const int threads = 256, grid = (c->nsens * 32 + threads - 1) / threads;
   dgk::sensor_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], c->dsel, c->dsw, c->nsens, c->Np, c->gamma, out);
@@ -208,7 +249,8 @@ dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st)
   A.dt = dt;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, launch_stage<dgk::MODE_UPDATE>(c->N, A, st));
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, st)
+                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, st));
     ++c->launches;
   }
   return DG_OK;
@@ -260,7 +302,7 @@ size_t dg_workspace_bytes(const dg_ctx* c) {
   b += align256(st);                                               // staging
   b += align256(size_t(c->K) * dgk::GEO * 8);                      // geo
   b += align256(size_t(c->K) * 16) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 8);
-  b += align256(c->opfrag.size() * 8) + align256(2 * 96 * c->Nfp + 4 * c->Nfp);
+  b += align256(op_host(c).size() * 8) + align256(2 * 96 * c->Nfp + 4 * c->Nfp);
   const size_t rec = size_t(5) * c->Nfp * 8;
   b += align256(c->nsend * rec) + align256(c->nrecv * rec) + align256(c->nsend * 4) + align256(c->nsend);
   b += align256(64) + align256(4096 * 8);
@@ -277,7 +319,7 @@ dg_status dg_memory_report(const dg_ctx* c, size_t bytes[7]) {
   bytes[2] = st;
   bytes[3] = size_t(c->K) * dgk::GEO * 8;
   bytes[4] = size_t(c->K) * (16 + 4 + 4 + 8);
-  bytes[5] = c->opfrag.size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp + size_t(DG_MAX_SENSORS) * (c->Np * 8 + 4);
+  bytes[5] = op_host(c).size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp + size_t(DG_MAX_SENSORS) * (c->Np * 8 + 4);
   bytes[6] = (c->nsend + c->nrecv) * rec + c->nsend * 5;
   return DG_OK;
 }
@@ -305,7 +347,7 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   c->dcode = reinterpret_cast<uint8_t*>(take(size_t(c->K) * 4));
   c->dpub = reinterpret_cast<int32_t*>(take(size_t(c->K) * 4));
   c->dgid = reinterpret_cast<int64_t*>(take(size_t(c->K) * 8));
-  c->dop = reinterpret_cast<double*>(take(c->opfrag.size() * 8));
+  c->dop = reinterpret_cast<double*>(take(op_host(c).size() * 8));
   c->dtbl = reinterpret_cast<uint8_t*>(take(2 * 96 * c->Nfp + 4 * c->Nfp));
   const size_t rec = size_t(5) * c->Nfp * 8;
   c->dsend = reinterpret_cast<double*>(take(c->nsend * rec));
@@ -325,7 +367,7 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   CUDA_TRY(c, cudaMemcpyAsync(c->dcode, c->code.data(), c->code.size(), cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(c->dpub, c->pub.data(), c->pub.size() * 4, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(c->dgid, c->gid.data(), c->gid.size() * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(c, cudaMemcpyAsync(c->dop, c->opfrag.data(), c->opfrag.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dop, op_host(c).data(), op_host(c).size() * 8, cudaMemcpyHostToDevice, st));
   std::vector<uint8_t>& tb = c->tbl;  // concatenated tables live until the copy completes (synced below)
   std::vector<uint8_t> all(tb);
   all.insert(all.end(), c->tblf.begin(), c->tblf.end());
@@ -370,6 +412,10 @@ dg_status dg_set_state(dg_ctx* c, const double* rho, const double* mx, const dou
   dgk::to_internal_kernel<<<grid, threads, 0, st>>>(c->dstage, c->dpub, c->dQ[0], c->dres, c->K, c->Np);
   ++c->launches;
   CUDA_TRY(c, cudaGetLastError());
+  if (c->scheme == DG_SCHEME_MODAL) {   // nodal values -> coefficients (interpolation, reading A23)
+    CUDA_TRY(c, modal_convert(c, c->dQ[0], c->dQ[1], true, st));
+    c->cur = 1;
+  }
   CUDA_TRY(c, cudaMemsetAsync(c->dflag, 0, 64, st));
   c->t = t;
   c->state_set = true;
@@ -386,7 +432,12 @@ dg_status dg_get_state(dg_ctx* c, double* rho, double* mx, double* my, double* m
   const size_t n = size_t(c->K) * c->Np;
   const int threads = 256;
   const int grid = int(std::min<int64_t>((int64_t(n) * 5 + threads - 1) / threads, 16 * num_sms()));
-  dgk::to_public_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], c->dpub, c->dstage, c->K, c->Np);
+  const double* src = c->dQ[c->cur];
+  if (c->scheme == DG_SCHEME_MODAL) {   // coefficients -> nodal values, in the spare state buffer
+    CUDA_TRY(c, modal_convert(c, c->dQ[c->cur], c->dQ[c->cur ^ 1], false, st));
+    src = c->dQ[c->cur ^ 1];
+  }
+  dgk::to_public_kernel<<<grid, threads, 0, st>>>(src, c->dpub, c->dstage, c->K, c->Np);
   ++c->launches;
   CUDA_TRY(c, cudaGetLastError());
   double* dst[5] = {rho, mx, my, mz, E};
@@ -426,7 +477,8 @@ dg_status dg_rhs_compute(dg_ctx* c, double t, double* out, int which, void* stre
   A.out = out;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, launch_stage<dgk::MODE_RHS>(c->N, A, st));
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, st)
+                                             : launch_stage<dgk::MODE_RHS>(c->N, A, st));
     ++c->launches;
   }
   return DG_OK;
@@ -516,7 +568,12 @@ dg_status dg_stable_dt(dg_ctx* c, double cfl, double* dt, void* stream) {
   const int64_t nn = c->K * c->Np;
   const int threads = 256;
   const int grid = int(std::min<int64_t>((nn + threads - 1) / threads, 4096));
-  dgk::max_speed_kernel<<<grid, threads, 0, st>>>(c->dQ[c->cur], nn, c->Np, c->gamma, c->dscratch);
+  const double* q = c->dQ[c->cur];
+  if (c->scheme == DG_SCHEME_MODAL) {   // wave speeds at the nodes
+    CUDA_TRY(c, modal_convert(c, c->dQ[c->cur], c->dQ[c->cur ^ 1], false, st));
+    q = c->dQ[c->cur ^ 1];
+  }
+  dgk::max_speed_kernel<<<grid, threads, 0, st>>>(q, nn, c->Np, c->gamma, c->dscratch);
   ++c->launches;
   CUDA_TRY(c, cudaGetLastError());
   std::vector<double> part(grid);
@@ -723,7 +780,18 @@ dg_status dg_sensors_set(dg_ctx* c, int n, const double* xyz, int32_t* elem_out,
   c->sens_elem = el;
   c->sens_w.assign(size_t(n) * Np, 0.0);
   for (int i = 0; i < n; ++i) {
-    if (el[i] >= 0) dgb::interp_weights(c->ref, rst[3 * i], rst[3 * i + 1], rst[3 * i + 2], &c->sens_w[size_t(i) * Np]);
+    if (el[i] >= 0) {
+      double* w = &c->sens_w[size_t(i) * Np];
+      dgb::interp_weights(c->ref, rst[3 * i], rst[3 * i + 1], rst[3 * i + 2], w);
+      if (c->scheme == DG_SCHEME_MODAL) {   // the state is coefficients: weights psi_m = sum_n l_n V_nm
+        std::vector<double> l(w, w + Np);
+        for (int mm = 0; mm < Np; ++mm) {
+          double acc = 0;
+          for (int nn = 0; nn < Np; ++nn) acc += l[nn] * c->modal.V[size_t(nn) * Np + mm];
+          w[mm] = acc;
+        }
+      }
+    }
     if (elem_out) elem_out[i] = el[i] >= 0 ? c->pub[el[i]] : -1;
   }
   dg_status e = upload_sensors(c, static_cast<cudaStream_t>(stream));   // or at dg_bind_workspace

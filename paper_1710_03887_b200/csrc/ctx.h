@@ -21,7 +21,10 @@ struct dg_ctx {
   double q_inf[5] = {1.4, 0, 0, 0, 2.5};
   int lambda_mode = 0, check_every = 0, rk_scheme = DG_RK_LSERK4;
   double inflow_alpha = 565.0;
+  int scheme = DG_SCHEME_NODAL;
   dgb::RefElem ref;
+  dgb::ModalTables modal;           // scheme == DG_SCHEME_MODAL
+  std::vector<double> modal_cat;    // concatenated tables (kernels.cuh MS<P> offsets)
 
   // ---- this rank's elements, internal order: interior first, then partition-boundary
   int64_t K = 0, K_int = 0;

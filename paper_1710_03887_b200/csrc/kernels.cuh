@@ -35,6 +35,7 @@ namespace dgk {
 constexpr int GEO = 25;          // 9 metric terms + 4 faces x (nx, ny, nz, Fscale)
 constexpr int CODE_GHOST = 32;   // 32 + f2*6 + sigma : neighbour trace in the halo buffer
 constexpr int CODE_BC = 64;      // 64 + tag          : physical boundary
+__device__ constexpr int PERM_INV[6] = {0, 1, 2, 4, 3, 5};   // inverse of the face-vertex permutations
 
 struct StageArgs {
   const double* Qin;      // [K][5][Np]
@@ -46,7 +47,7 @@ struct StageArgs {
   const uint8_t* code;    // [K][4]
   const int* pub;         // [K] public index
   const double* recv;     // [nrecv][5][Nfp]
-  const double* op;       // B fragments
+  const double* op;       // B fragments (nodal) / concatenated modal tables (modal scheme)
   const uint8_t* tbl;     // [4][4][6][Nfp] neighbour volume node  (local neighbours)
   const uint8_t* tblf;    // [4][4][6][Nfp] neighbour face-local node (halo records)
   const uint8_t* fmask;   // [4][Nfp]
@@ -1260,6 +1261,231 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     }
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------- modal-quadrature scheme (N3)
+// The paper's own discretisation (Appendix A; reading A23):
+// unknowns are coefficients of the orthonormal basis psi, the weak form is integrated by
+// collapsed Gauss-Jacobi rules with p+1 points per direction (degree 2p+1) on the tet and on
+// each face, every face at the points of its owner (smaller global element id):
+//   dc_i/dt = sum_q w_q sum_a dpsi_i/dxi_a(q) Ft_a(u(q)) - sum_f Fscale_f sum_q w^f_q psi_i(q) F*_n(q).
+// One CTA per tile of EB elements, phases separated by __syncthreads; tables (ModalTables,
+// concatenated) read through the L1.
+template <int P>
+struct MS {
+  static constexpr int NP = (P + 1) * (P + 2) * (P + 3) / 6, NQ1 = P + 1;
+  static constexpr int NQ = NQ1 * NQ1 * NQ1, NQF = NQ1 * NQ1;
+  static constexpr int EB = P <= 2 ? 8 : 4, NT = 256;
+  // table offsets (doubles) in the concatenation of refelem.h ModalTables
+  static constexpr int O_WQ = 0, O_VQ = O_WQ + NQ, O_DQ = O_VQ + NQ * NP, O_WF = O_DQ + 3 * NP * NQ;
+  static constexpr int O_PSTD = O_WF + NQF, O_PMAP = O_PSTD + 4 * NQF * NP, O_V = O_PMAP + 96 * NQF * NP;
+  static constexpr int O_VINV = O_V + NP * NP, TOTAL = O_VINV + NP * NP;
+  // shared memory (doubles); the volume fluxes of one element are padded to an odd stride so
+  // the projection's element-parallel reads hit distinct banks
+  static constexpr int FVS = 3 * 5 * NQ + 1;
+  static constexpr int S_C = 0, S_FV = S_C + EB * 5 * NP, S_UM = S_FV + EB * FVS,
+                       S_UP = S_UM + EB * 4 * 5 * NQF, S_LAM = S_UP + EB * 4 * 5 * NQF, S_CN = S_LAM + EB * 4 * NQF,
+                       S_END = S_CN + EB * 4 * 5 * NP;
+  static_assert(EB * 5 * NP <= EB * 4 * 5 * NQF, "rhs staging reuses the exterior-trace buffer");
+  static constexpr size_t SMEM = size_t(S_END) * 8 + size_t(EB) * 4 * 4 * 3;   // + own-table offsets, nbr, code
+};
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(MS<P>::NT) modal_stage_kernel(const StageArgs A) {
+  using M = MS<P>;
+  constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF, EB = M::EB, NT = M::NT, FVS = M::FVS;
+  extern __shared__ __align__(16) double sm[];
+  double* c_s = sm + M::S_C;      // [EB][5][NP]
+  double* fv_s = sm + M::S_FV;    // [EB][3][5][NQ] (element stride FVS)
+  double* um_s = sm + M::S_UM;    // [EB][4][5][NQF]; later the weighted fluxes Fscale w F*
+  double* up_s = sm + M::S_UP;    // [EB][4][5][NQF]; later the rhs staging [EB][5][NP]
+  double* lam_s = sm + M::S_LAM;  // [EB][4][NQF]
+  double* cn_s = sm + M::S_CN;    // [EB][4][5][NP] neighbour coefficients
+  int* own_s = reinterpret_cast<int*>(sm + M::S_END);   // [EB][4] offset of the own-side face table
+  int* nb_s = own_s + EB * 4;                            // [EB][4] neighbour element
+  int* cd_s = nb_s + EB * 4;                             // [EB][4] face code
+  const double* T = A.op;
+  const int tid = threadIdx.x;
+  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+  const int e0 = A.e_begin + blockIdx.x * EB;
+  const int ne = min(EB, A.e_end - e0);
+  if (ne <= 0) return;
+  for (int i = tid; i < ne * 4; i += NT) {
+    nb_s[i] = A.nbr[size_t(e0) * 4 + i];
+    cd_s[i] = A.code[size_t(e0) * 4 + i];
+  }
+  for (int i = tid; i < ne * 5 * NP; i += NT) c_s[i] = A.Qin[size_t(e0) * 5 * NP + i];
+  __syncthreads();
+  // neighbour coefficients of every paired face, once per face (boundary faces: unused)
+#pragma unroll 4
+  for (int i = tid; i < ne * 4 * 5 * NP; i += NT) {
+    const int ef = i / (5 * NP), r0 = i - ef * 5 * NP;
+    cn_s[i] = cd_s[ef] < CODE_GHOST ? __ldg(A.Qin + size_t(nb_s[ef]) * 5 * NP + r0) : 0.0;
+  }
+  __syncthreads();
+  // ---- volume: u at the quadrature points, contravariant fluxes (threads of a warp share q)
+  for (int idx = tid; idx < ne * NQ; idx += NT) {
+    const int q = idx / ne, e = idx - q * ne;
+    double u[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      double acc = 0;
+      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_VQ + q * NP + i), c_s[(e * 5 + c) * NP + i], acc);
+      u[c] = acc;
+    }
+    const double ri = 1.0 / u[0];
+    const double vx = u[1] * ri, vy = u[2] * ri, vz = u[3] * ri;
+    const double p = gm1 * (u[4] - 0.5 * (u[1] * vx + u[2] * vy + u[3] * vz));
+    if (!state_ok(u[0], p, u[1], u[2], u[3], u[4])) flag_blowup(A.flag, A.gid[e0 + e]);
+    const double* G = A.geo + size_t(e0 + e) * GEO;
+    const double pd = p - A.pref, Ep = u[4] + p;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double cx = G[3 * a], cy = G[3 * a + 1], cz = G[3 * a + 2];
+      const double U = cx * vx + cy * vy + cz * vz;
+      double* o = fv_s + e * FVS + (a * 5) * NQ + q;
+      o[0] = u[0] * U;
+      o[NQ] = fma(cx, pd, u[1] * U);
+      o[2 * NQ] = fma(cy, pd, u[2] * U);
+      o[3 * NQ] = fma(cz, pd, u[3] * U);
+      o[4 * NQ] = Ep * U;
+    }
+  }
+  // ---- faces: both traces at the owner's points, node speeds
+  for (int idx = tid; idx < ne * 4 * NQF; idx += NT) {
+    const int fq = idx / ne, e = idx - fq * ne, f = fq / NQF, q = fq - f * NQF;
+    const int k = e0 + e;
+    const int code = cd_s[e * 4 + f], nb = nb_s[e * 4 + f];
+    const double* G = A.geo + size_t(k) * GEO + 9 + 4 * f;
+    const double nx = G[0], ny = G[1], nz = G[2];
+    int own_off = M::O_PSTD + f * NQF * NP, nb_off = 0;
+    if (code < CODE_GHOST) {
+      const int f2 = code / 6, sg = code - 6 * f2;
+      if (A.gid[k] < A.gid[nb]) {
+        nb_off = M::O_PMAP + ((f * 4 + f2) * 6 + sg) * NQF * NP;
+      } else {
+        own_off = M::O_PMAP + ((f2 * 4 + f) * 6 + PERM_INV[sg]) * NQF * NP;
+        nb_off = M::O_PSTD + f2 * NQF * NP;
+      }
+    }
+    if (q == 0) own_s[e * 4 + f] = own_off;
+    double um[5], up[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      double acc = 0;
+      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + own_off + q * NP + i), c_s[(e * 5 + c) * NP + i], acc);
+      um[c] = acc;
+    }
+    if (code < CODE_GHOST) {
+      const double* cn = cn_s + ((e * 4 + f) * 5) * NP;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        double acc = 0;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + nb_off + q * NP + i), cn[c * NP + i], acc);
+        up[c] = acc;
+      }
+    } else {
+      ghost_trace(A, code - CODE_BC, um, nx, ny, nz, up);
+    }
+    double* om = um_s + ((e * 4 + f) * 5) * NQF + q;
+    double* op = up_s + ((e * 4 + f) * 5) * NQF + q;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      om[c * NQF] = um[c];
+      op[c * NQF] = up[c];
+    }
+    auto speed = [&](const double* w) {
+      const double ri = 1.0 / w[0];
+      const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
+      const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+      return fabs(un) + sqrt(gamma * p * ri);
+    };
+    lam_s[(e * 4 + f) * NQF + q] = fmax(speed(um), speed(up));
+  }
+  __syncthreads();
+  // ---- LLF flux at the face points, weighted by Fscale w_q, in place of the interior trace
+  for (int idx = tid; idx < ne * 4 * NQF; idx += NT) {
+    const int fq = idx / ne, e = idx - fq * ne, f = fq / NQF, q = fq - f * NQF;
+    const double* G = A.geo + size_t(e0 + e) * GEO + 9 + 4 * f;
+    const double nx = G[0], ny = G[1], nz = G[2];
+    double lam = lam_s[(e * 4 + f) * NQF + q];
+    if (A.lambda_mode == 0)
+      for (int qq = 0; qq < NQF; ++qq) lam = fmax(lam, lam_s[(e * 4 + f) * NQF + qq]);
+    double* om = um_s + ((e * 4 + f) * 5) * NQF + q;
+    const double* op = up_s + ((e * 4 + f) * 5) * NQF + q;
+    double um[5], up[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      um[c] = om[c * NQF];
+      up[c] = op[c * NQF];
+    }
+    auto nflux = [&](const double* w, double* fo) {
+      const double ri = 1.0 / w[0];
+      const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
+      const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+      const double pd = p - A.pref;
+      fo[0] = w[0] * un;
+      fo[1] = fma(pd, nx, w[1] * un);
+      fo[2] = fma(pd, ny, w[2] * un);
+      fo[3] = fma(pd, nz, w[3] * un);
+      fo[4] = (w[4] + p) * un;
+    };
+    double fm[5], fp[5];
+    nflux(um, fm);
+    nflux(up, fp);
+    const double sc = G[3] * __ldg(T + M::O_WF + q);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) om[c * NQF] = sc * (0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]));
+  }
+  __syncthreads();
+  // ---- projection onto the basis and the RK update (or rhs out); threads of a warp share (c, i)
+  double* r_s = up_s;
+  for (int idx = tid; idx < ne * 5 * NP; idx += NT) {
+    const int ci = idx / ne, e = idx - ci * ne, c = ci / NP, i = ci - c * NP;
+    double acc = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double* D = T + M::O_DQ + (a * NP + i) * NQ;
+      const double* F = fv_s + e * FVS + (a * 5 + c) * NQ;
+      for (int q = 0; q < NQ; ++q) acc = fma(__ldg(D + q), F[q], acc);
+    }
+    for (int f = 0; f < 4; ++f) {
+      const double* Pt = T + own_s[e * 4 + f];
+      const double* F = um_s + ((e * 4 + f) * 5 + c) * NQF;
+      for (int q = 0; q < NQF; ++q) acc = fma(-__ldg(Pt + q * NP + i), F[q], acc);
+    }
+    const int li = (e * 5 + c) * NP + i;
+    if (MODE == MODE_UPDATE) {
+      const size_t gi = size_t(e0) * 5 * NP + li;
+      const double rr = fma(A.a, A.res[gi], A.dt * acc);
+      A.res[gi] = rr;
+      A.Qout[gi] = fma(A.b, rr, c_s[li]);
+    } else {
+      r_s[li] = acc;
+    }
+  }
+  if (MODE == MODE_RHS) {   // public rhs as nodal values: V (dc/dt)
+    __syncthreads();
+    for (int idx = tid; idx < ne * 5 * NP; idx += NT) {
+      const int cn = idx / ne, e = idx - cn * ne, c = cn / NP, n = cn - c * NP;
+      double acc = 0;
+      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), r_s[(e * 5 + c) * NP + i], acc);
+      A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = acc;
+    }
+  }
+}
+
+// nodal values <-> modal coefficients per element and field: out = Mat (NP x NP) in
+__global__ void modal_convert_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                     const double* __restrict__ Mat, int64_t K, int NP) {
+  const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (idx >= K * 5 * NP) return;
+  const int64_t row = idx / NP;
+  const int n = int(idx - row * NP);
+  const double* x = in + row * NP;
+  double acc = 0;
+  for (int i = 0; i < NP; ++i) acc = fma(Mat[n * NP + i], x[i], acc);
+  out[idx] = acc;
 }
 
 // pack the traces of this rank's partition faces: send[s][c][j] = Q[k][c][Fmask_f[j]]

@@ -62,6 +62,16 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   c->inflow_alpha = d->inflow_alpha > 0 ? d->inflow_alpha : 565.0;
   std::string msg;
   if (!build_reference(c->N, c->ref, &msg)) return fail(c, DG_EARG, "reference element: " + msg);
+  if (d->scheme != DG_SCHEME_NODAL && d->scheme != DG_SCHEME_MODAL) return fail(c, DG_EARG, "unknown scheme");
+  c->scheme = d->scheme;
+  if (c->scheme == DG_SCHEME_MODAL) {
+    if (c->N > 3) return fail(c, DG_EUNSUPPORTED, "the modal scheme is built for orders 1-3");
+    if (nparts > 1) return fail(c, DG_EUNSUPPORTED, "the modal scheme runs on one partition");
+    if (!build_modal(c->ref, c->modal, &msg)) return fail(c, DG_EARG, "modal tables: " + msg);
+    const ModalTables& T = c->modal;
+    for (const std::vector<double>* v : {&T.wq, &T.Vq, &T.Dq, &T.wf, &T.Pstd, &T.Pmap, &T.V, &T.Vinv})
+      c->modal_cat.insert(c->modal_cat.end(), v->begin(), v->end());
+  }
   const int N = c->N, Np = c->ref.Np, Nfp = c->ref.Nfp;
   c->Np = Np;
   c->Nfp = Nfp;

@@ -366,4 +366,129 @@ void interp_weights(const RefElem& R, double r, double s, double t, double* w) {
   }
 }
 
+// ---------------------------------------------------------------- modal scheme (N3)
+namespace {
+// n-point Gauss-Jacobi rule for the weight (1-x)^alpha: Newton on the orthonormal Jacobi
+// polynomial from Chebyshev guesses (with deflation), Christoffel weights 1/sum_k p_k(x)^2
+void gauss_jacobi(int n, double alpha, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    double r = -std::cos((2.0 * k + 1) * M_PI / (2.0 * n));
+    if (k > 0) r = 0.5 * (r + x[k - 1]);
+    for (int it = 0; it < 200; ++it) {
+      double f = jacobi(r, alpha, 0, n), df = djacobi(r, alpha, 0, n), s = 0;
+      for (int i = 0; i < k; ++i) s += 1.0 / (r - x[i]);
+      const double dr = f / (df - s * f);
+      r -= dr;
+      if (std::fabs(dr) < 1e-16) break;
+    }
+    x[k] = r;
+  }
+  std::sort(x.begin(), x.end());
+  for (int k = 0; k < n; ++k) {
+    double s = 0;
+    for (int j = 0; j < n; ++j) {
+      const double pj = jacobi(x[k], alpha, 0, j);
+      s += pj * pj;
+    }
+    w[k] = 1.0 / s;
+  }
+}
+
+void face_point(int f, double u, double v, double& r, double& s, double& t) {
+  switch (f) {
+    case 0: r = u; s = v; t = -1; break;
+    case 1: r = u; s = -1; t = v; break;
+    case 2: r = -1 - u - v; s = u; t = v; break;
+    default: r = -1; s = u; t = v; break;
+  }
+}
+
+const double REFV[4][3] = {{-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {-1, -1, 1}};
+
+void psi_row(const RefElem& R, double r, double s, double t, double* out, double* dr = nullptr, double* ds = nullptr,
+             double* dt = nullptr) {
+  int m = 0;
+  for (int i = 0; i <= R.N; ++i)
+    for (int j = 0; j <= R.N - i; ++j)
+      for (int k = 0; k <= R.N - i - j; ++k, ++m) {
+        double v, a, b, c;
+        pkdo3(r, s, t, i, j, k, v, a, b, c);
+        out[m] = v;
+        if (dr) { dr[m] = a; ds[m] = b; dt[m] = c; }
+      }
+}
+}  // namespace
+
+const int PERM6_INV[6] = {0, 1, 2, 4, 3, 5};
+
+bool build_modal(const RefElem& R, ModalTables& T, std::string* msg) {
+  const int p = R.N, Np = R.Np, n = p + 1;
+  T.p = p;
+  T.Np = Np;
+  std::vector<double> ga, wa, gb, wb, gc, wc;
+  gauss_jacobi(n, 0, ga, wa);
+  gauss_jacobi(n, 1, gb, wb);
+  gauss_jacobi(n, 2, gc, wc);
+  // orthonormal Jacobi weights integrate 1 to the weight's integral: check sum(wa) = 2
+  double sa = 0;
+  for (double v : wa) sa += v;
+  if (std::fabs(sa - 2.0) > 1e-12) { if (msg) *msg = "Gauss-Jacobi rule"; return false; }
+  T.NQ = n * n * n;
+  T.NQF = n * n;
+  T.wq.resize(T.NQ);
+  T.Vq.assign(size_t(T.NQ) * Np, 0.0);
+  T.Dq.assign(size_t(3) * Np * T.NQ, 0.0);
+  std::vector<double> v(Np), dr(Np), ds(Np), dt(Np);
+  int q = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k, ++q) {
+        const double a = ga[i], b = gb[j], c = gc[k];
+        const double r = (1 + a) * (1 - b) * (1 - c) / 4 - 1, s = (1 + b) * (1 - c) / 2 - 1, t = c;
+        T.wq[q] = wa[i] * wb[j] * wc[k] / 8;
+        psi_row(R, r, s, t, v.data(), dr.data(), ds.data(), dt.data());
+        for (int m = 0; m < Np; ++m) {
+          T.Vq[size_t(q) * Np + m] = v[m];
+          T.Dq[(size_t(0) * Np + m) * T.NQ + q] = T.wq[q] * dr[m];
+          T.Dq[(size_t(1) * Np + m) * T.NQ + q] = T.wq[q] * ds[m];
+          T.Dq[(size_t(2) * Np + m) * T.NQ + q] = T.wq[q] * dt[m];
+        }
+      }
+  // face rule in the parameter (u, v), and the face barycentrics of its points
+  std::vector<double> fu(T.NQF), fv(T.NQF);
+  T.wf.resize(T.NQF);
+  q = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j, ++q) {
+      fu[q] = (1 + ga[i]) * (1 - gb[j]) / 2 - 1;
+      fv[q] = gb[j];
+      T.wf[q] = wa[i] * wb[j] / 2;
+    }
+  T.Pstd.assign(size_t(4) * T.NQF * Np, 0.0);
+  T.Pmap.assign(size_t(96) * T.NQF * Np, 0.0);
+  for (int fa = 0; fa < 4; ++fa)
+    for (int qq = 0; qq < T.NQF; ++qq) {
+      double r, s, t;
+      face_point(fa, fu[qq], fv[qq], r, s, t);
+      psi_row(R, r, s, t, &T.Pstd[(size_t(fa) * T.NQF + qq) * Np]);
+      // barycentrics over the tet vertices, then over face fa's vertices
+      const double lam[4] = {-(1 + r + s + t) / 2, (1 + r) / 2, (1 + s) / 2, (1 + t) / 2};
+      double beta[3];
+      for (int mm = 0; mm < 3; ++mm) beta[mm] = lam[FACE_VERTS[fa][mm]];
+      for (int fb = 0; fb < 4; ++fb)
+        for (int sg = 0; sg < 6; ++sg) {
+          double x[3] = {0, 0, 0};
+          for (int mm = 0; mm < 3; ++mm)
+            for (int d = 0; d < 3; ++d) x[d] += beta[mm] * REFV[FACE_VERTS[fb][PERM6[sg][mm]]][d];
+          psi_row(R, x[0], x[1], x[2], &T.Pmap[((size_t(fa * 4 + fb) * 6 + sg) * T.NQF + qq) * Np]);
+        }
+    }
+  T.V.assign(size_t(Np) * Np, 0.0);
+  for (int nn = 0; nn < Np; ++nn) psi_row(R, R.r[nn], R.s[nn], R.t[nn], &T.V[size_t(nn) * Np]);
+  T.Vinv = R.Vinv;
+  return true;
+}
+
 }  // namespace dgb

@@ -35,6 +35,26 @@ inline int n_face_nodes(int N) { return (N + 1) * (N + 2) / 2; }
 // Builds everything above; returns false (with msg) on numerical failure.
 bool build_reference(int N, RefElem& R, std::string* msg);
 
+// Tables of the paper's modal-quadrature scheme (reading A23):
+// orthonormal PKDO basis psi (the same polynomials as the nodal operators), collapsed
+// Gauss-Jacobi rules with n = p+1 points per direction (exact to degree 2p+1) on the tet
+// and on each face triangle.  Face points are those of the face's owner (smaller global
+// element id): Pstd[f] evaluates psi at the standard rule of face f, Pmap[fa][fb][sigma] at
+// the standard points of face fa carried onto face fb when face vertex m of fa matches
+// face vertex PERM6[sigma][m] of fb.
+struct ModalTables {
+  int p = 0, Np = 0, NQ = 0, NQF = 0;
+  std::vector<double> wq;               // NQ volume weights
+  std::vector<double> Vq;               // NQ x Np   psi at the volume points
+  std::vector<double> Dq;               // 3 x Np x NQ   w_q dpsi_i/d(r,s,t)
+  std::vector<double> wf;               // NQF face weights (parameter measure, area 2)
+  std::vector<double> Pstd;             // 4 x NQF x Np
+  std::vector<double> Pmap;             // 4 x 4 x 6 x NQF x Np
+  std::vector<double> V, Vinv;          // Np x Np nodal <-> modal (V_nm = psi_m(x_n))
+};
+bool build_modal(const RefElem& R, ModalTables& T, std::string* msg);
+extern const int PERM6_INV[6];
+
 // Nodal interpolation weights at a reference point: w_i = l_i(r,s,t) = sum_j Vinv[j][i] psi_j(r,s,t).
 void interp_weights(const RefElem& R, double r, double s, double t, double* w);
 

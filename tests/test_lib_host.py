@@ -179,3 +179,19 @@ def test_partition_halo_lists_pair_up(nparts):
     finally:
         for c in ctxs:
             dg.dg_destroy(c)
+
+
+def test_modal_scheme_limits():
+    """DG_SCHEME_MODAL: orders 1-3 on one partition (include/dg.h); others refused."""
+    m = smesh.kuhn_box((2, 2, 2), (0, 0, 0), (1, 1, 1))
+    for N in (1, 2, 3):
+        dg.dg_destroy(dg.dg_mesh_create(N, m.vxyz, m.etov, m.bc, scheme=dg.DG_SCHEME_MODAL))
+    with pytest.raises(dg.DGError) as e:
+        dg.dg_mesh_create(4, m.vxyz, m.etov, m.bc, scheme=dg.DG_SCHEME_MODAL)
+    assert e.value.status == dg.DG_EUNSUPPORTED
+    part = (np.arange(m.K) % 2).astype(np.int32)
+    with pytest.raises(dg.DGError) as e:
+        dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc, part=part, nparts=2, scheme=dg.DG_SCHEME_MODAL)
+    assert e.value.status == dg.DG_EUNSUPPORTED
+    with pytest.raises(dg.DGError):
+        dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc, scheme=7)
