@@ -137,16 +137,17 @@ const std::vector<double>& op_host(const dg_ctx* c) { return c->scheme == DG_SCH
 
 template <int P, int MODE>
 cudaError_t launch_modal_p(const dgk::StageArgs& A, cudaStream_t st) {
-  using M = dgk::MS<P>;
+  using W = dgk::MW<P>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgk::modal_stage_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(M::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(dgk::modal_warp_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int ntiles = (A.e_end - A.e_begin + M::EB - 1) / M::EB;
-  if (ntiles <= 0) return cudaSuccess;
-  dgk::modal_stage_kernel<P, MODE><<<ntiles, M::NT, M::SMEM, st>>>(A);
+  const int nel = A.e_end - A.e_begin;
+  if (nel <= 0) return cudaSuccess;
+  const int grid = std::min((nel + W::WPC - 1) / W::WPC, 8 * num_sms());
+  dgk::modal_warp_kernel<P, MODE><<<grid, W::NT, W::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -1269,209 +1269,209 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
 // collapsed Gauss-Jacobi rules with p+1 points per direction (degree 2p+1) on the tet and on
 // each face, every face at the points of its owner (smaller global element id):
 //   dc_i/dt = sum_q w_q sum_a dpsi_i/dxi_a(q) Ft_a(u(q)) - sum_f Fscale_f sum_q w^f_q psi_i(q) F*_n(q).
-// One CTA per tile of EB elements, phases separated by __syncthreads; tables (ModalTables,
-// concatenated) read through the L1.
+// Tables (ModalTables, concatenated; MS<P> offsets) are read through the L1.
 template <int P>
 struct MS {
   static constexpr int NP = (P + 1) * (P + 2) * (P + 3) / 6, NQ1 = P + 1;
   static constexpr int NQ = NQ1 * NQ1 * NQ1, NQF = NQ1 * NQ1;
-  static constexpr int EB = P <= 2 ? 8 : 4, NT = 256;
   // table offsets (doubles) in the concatenation of refelem.h ModalTables
   static constexpr int O_WQ = 0, O_VQ = O_WQ + NQ, O_DQ = O_VQ + NQ * NP, O_WF = O_DQ + 3 * NP * NQ;
   static constexpr int O_PSTD = O_WF + NQF, O_PMAP = O_PSTD + 4 * NQF * NP, O_V = O_PMAP + 96 * NQF * NP;
   static constexpr int O_VINV = O_V + NP * NP, TOTAL = O_VINV + NP * NP;
-  // shared memory (doubles); the volume fluxes of one element are padded to an odd stride so
-  // the projection's element-parallel reads hit distinct banks
-  static constexpr int FVS = 3 * 5 * NQ + 1;
-  static constexpr int S_C = 0, S_FV = S_C + EB * 5 * NP, S_UM = S_FV + EB * FVS,
-                       S_UP = S_UM + EB * 4 * 5 * NQF, S_LAM = S_UP + EB * 4 * 5 * NQF, S_CN = S_LAM + EB * 4 * NQF,
-                       S_END = S_CN + EB * 4 * 5 * NP;
-  static_assert(EB * 5 * NP <= EB * 4 * 5 * NQF, "rhs staging reuses the exterior-trace buffer");
-  static constexpr size_t SMEM = size_t(S_END) * 8 + size_t(EB) * 4 * 4 * 3;   // + own-table offsets, nbr, code
+};
+
+// Each warp owns one element at a time (persistent CTAs, warps stride over the elements), its coefficients, its
+// neighbours' coefficients and its quadrature values in a private slice of shared memory;
+// lanes map to quadrature points for the interpolations and fluxes and to (field, mode)
+// pairs for the projections; only __syncwarp between the steps.
+template <int P>
+struct MW {
+  using M = MS<P>;
+  static constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF;
+  static constexpr int WPC = P <= 2 ? 8 : 4, NT = 32 * WPC;           // warps per CTA
+  static constexpr int MINB = P == 1 ? 4 : P == 2 ? 2 : 1;             // CTAs per SM (register cap)
+  static constexpr int W_C = 0, W_CN = W_C + 5 * NP, W_FV = W_CN + 4 * 5 * NP, W_LAM = W_FV + 15 * NQ,
+                       W_FS = W_LAM + 4 * NQF, W_END = W_FS + 5 * 4 * NQF;
+  static constexpr int WSTRIDE = W_END + 1;                            // doubles per warp (odd)
+  static constexpr size_t SMEM = size_t(WPC) * WSTRIDE * 8 + size_t(WPC) * 4 * 4;
 };
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(MS<P>::NT) modal_stage_kernel(const StageArgs A) {
+__global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(const StageArgs A) {
   using M = MS<P>;
-  constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF, EB = M::EB, NT = M::NT, FVS = M::FVS;
+  using W = MW<P>;
+  constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF;
   extern __shared__ __align__(16) double sm[];
-  double* c_s = sm + M::S_C;      // [EB][5][NP]
-  double* fv_s = sm + M::S_FV;    // [EB][3][5][NQ] (element stride FVS)
-  double* um_s = sm + M::S_UM;    // [EB][4][5][NQF]; later the weighted fluxes Fscale w F*
-  double* up_s = sm + M::S_UP;    // [EB][4][5][NQF]; later the rhs staging [EB][5][NP]
-  double* lam_s = sm + M::S_LAM;  // [EB][4][NQF]
-  double* cn_s = sm + M::S_CN;    // [EB][4][5][NP] neighbour coefficients
-  int* own_s = reinterpret_cast<int*>(sm + M::S_END);   // [EB][4] offset of the own-side face table
-  int* nb_s = own_s + EB * 4;                            // [EB][4] neighbour element
-  int* cd_s = nb_s + EB * 4;                             // [EB][4] face code
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ws = sm + warp * W::WSTRIDE;
+  double* c_s = ws + W::W_C;      // [5][NP]
+  double* cn_s = ws + W::W_CN;    // [4][5][NP]
+  double* fv_s = ws + W::W_FV;    // [3][5][NQ]
+  double* lam_s = ws + W::W_LAM;  // [4][NQF]
+  double* fs_s = ws + W::W_FS;    // [5][4][NQF]  Fscale w F*
+  int* own_s = reinterpret_cast<int*>(sm + W::WPC * W::WSTRIDE) + warp * 4;
   const double* T = A.op;
-  const int tid = threadIdx.x;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
-  const int e0 = A.e_begin + blockIdx.x * EB;
-  const int ne = min(EB, A.e_end - e0);
-  if (ne <= 0) return;
-  for (int i = tid; i < ne * 4; i += NT) {
-    nb_s[i] = A.nbr[size_t(e0) * 4 + i];
-    cd_s[i] = A.code[size_t(e0) * 4 + i];
-  }
-  for (int i = tid; i < ne * 5 * NP; i += NT) c_s[i] = A.Qin[size_t(e0) * 5 * NP + i];
-  __syncthreads();
-  // neighbour coefficients of every paired face, once per face (boundary faces: unused)
-#pragma unroll 4
-  for (int i = tid; i < ne * 4 * 5 * NP; i += NT) {
-    const int ef = i / (5 * NP), r0 = i - ef * 5 * NP;
-    cn_s[i] = cd_s[ef] < CODE_GHOST ? __ldg(A.Qin + size_t(nb_s[ef]) * 5 * NP + r0) : 0.0;
-  }
-  __syncthreads();
-  // ---- volume: u at the quadrature points, contravariant fluxes (threads of a warp share q)
-  for (int idx = tid; idx < ne * NQ; idx += NT) {
-    const int q = idx / ne, e = idx - q * ne;
-    double u[5];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      double acc = 0;
-      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_VQ + q * NP + i), c_s[(e * 5 + c) * NP + i], acc);
-      u[c] = acc;
+  const int nel = A.e_end - A.e_begin;
+  for (int el = blockIdx.x * W::WPC + warp; el < nel; el += gridDim.x * W::WPC) {
+    const int k = A.e_begin + el;
+    const double* G = A.geo + size_t(k) * GEO;
+    for (int i = lane; i < 5 * NP; i += 32) c_s[i] = A.Qin[size_t(k) * 5 * NP + i];
+    for (int i = lane; i < 4 * 5 * NP; i += 32) {
+      const int f = i / (5 * NP), r0 = i - f * 5 * NP;
+      const int code = A.code[size_t(k) * 4 + f];
+      cn_s[i] = code < CODE_GHOST ? __ldg(A.Qin + size_t(A.nbr[size_t(k) * 4 + f]) * 5 * NP + r0) : 0.0;
     }
-    const double ri = 1.0 / u[0];
-    const double vx = u[1] * ri, vy = u[2] * ri, vz = u[3] * ri;
-    const double p = gm1 * (u[4] - 0.5 * (u[1] * vx + u[2] * vy + u[3] * vz));
-    if (!state_ok(u[0], p, u[1], u[2], u[3], u[4])) flag_blowup(A.flag, A.gid[e0 + e]);
-    const double* G = A.geo + size_t(e0 + e) * GEO;
-    const double pd = p - A.pref, Ep = u[4] + p;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double cx = G[3 * a], cy = G[3 * a + 1], cz = G[3 * a + 2];
-      const double U = cx * vx + cy * vy + cz * vz;
-      double* o = fv_s + e * FVS + (a * 5) * NQ + q;
-      o[0] = u[0] * U;
-      o[NQ] = fma(cx, pd, u[1] * U);
-      o[2 * NQ] = fma(cy, pd, u[2] * U);
-      o[3 * NQ] = fma(cz, pd, u[3] * U);
-      o[4 * NQ] = Ep * U;
-    }
-  }
-  // ---- faces: both traces at the owner's points, node speeds
-  for (int idx = tid; idx < ne * 4 * NQF; idx += NT) {
-    const int fq = idx / ne, e = idx - fq * ne, f = fq / NQF, q = fq - f * NQF;
-    const int k = e0 + e;
-    const int code = cd_s[e * 4 + f], nb = nb_s[e * 4 + f];
-    const double* G = A.geo + size_t(k) * GEO + 9 + 4 * f;
-    const double nx = G[0], ny = G[1], nz = G[2];
-    int own_off = M::O_PSTD + f * NQF * NP, nb_off = 0;
-    if (code < CODE_GHOST) {
-      const int f2 = code / 6, sg = code - 6 * f2;
-      if (A.gid[k] < A.gid[nb]) {
-        nb_off = M::O_PMAP + ((f * 4 + f2) * 6 + sg) * NQF * NP;
-      } else {
-        own_off = M::O_PMAP + ((f2 * 4 + f) * 6 + PERM_INV[sg]) * NQF * NP;
-        nb_off = M::O_PSTD + f2 * NQF * NP;
-      }
-    }
-    if (q == 0) own_s[e * 4 + f] = own_off;
-    double um[5], up[5];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      double acc = 0;
-      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + own_off + q * NP + i), c_s[(e * 5 + c) * NP + i], acc);
-      um[c] = acc;
-    }
-    if (code < CODE_GHOST) {
-      const double* cn = cn_s + ((e * 4 + f) * 5) * NP;
+    __syncwarp();
+    // ---- volume points: values, validity, contravariant fluxes
+    for (int q = lane; q < NQ; q += 32) {
+      double u[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         double acc = 0;
-        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + nb_off + q * NP + i), cn[c * NP + i], acc);
-        up[c] = acc;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_VQ + q * NP + i), c_s[c * NP + i], acc);
+        u[c] = acc;
       }
-    } else {
-      ghost_trace(A, code - CODE_BC, um, nx, ny, nz, up);
-    }
-    double* om = um_s + ((e * 4 + f) * 5) * NQF + q;
-    double* op = up_s + ((e * 4 + f) * 5) * NQF + q;
+      const double ri = 1.0 / u[0];
+      const double vx = u[1] * ri, vy = u[2] * ri, vz = u[3] * ri;
+      const double p = gm1 * (u[4] - 0.5 * (u[1] * vx + u[2] * vy + u[3] * vz));
+      if (!state_ok(u[0], p, u[1], u[2], u[3], u[4])) flag_blowup(A.flag, A.gid[k]);
+      const double pd = p - A.pref, Ep = u[4] + p;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      om[c * NQF] = um[c];
-      op[c * NQF] = up[c];
+      for (int a = 0; a < 3; ++a) {
+        const double cx = G[3 * a], cy = G[3 * a + 1], cz = G[3 * a + 2];
+        const double U = cx * vx + cy * vy + cz * vz;
+        double* o = fv_s + (a * 5) * NQ + q;
+        o[0] = u[0] * U;
+        o[NQ] = fma(cx, pd, u[1] * U);
+        o[2 * NQ] = fma(cy, pd, u[2] * U);
+        o[3 * NQ] = fma(cz, pd, u[3] * U);
+        o[4 * NQ] = Ep * U;
+      }
     }
-    auto speed = [&](const double* w) {
-      const double ri = 1.0 / w[0];
-      const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
-      const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
-      return fabs(un) + sqrt(gamma * p * ri);
-    };
-    lam_s[(e * 4 + f) * NQF + q] = fmax(speed(um), speed(up));
-  }
-  __syncthreads();
-  // ---- LLF flux at the face points, weighted by Fscale w_q, in place of the interior trace
-  for (int idx = tid; idx < ne * 4 * NQF; idx += NT) {
-    const int fq = idx / ne, e = idx - fq * ne, f = fq / NQF, q = fq - f * NQF;
-    const double* G = A.geo + size_t(e0 + e) * GEO + 9 + 4 * f;
-    const double nx = G[0], ny = G[1], nz = G[2];
-    double lam = lam_s[(e * 4 + f) * NQF + q];
-    if (A.lambda_mode == 0)
-      for (int qq = 0; qq < NQF; ++qq) lam = fmax(lam, lam_s[(e * 4 + f) * NQF + qq]);
-    double* om = um_s + ((e * 4 + f) * 5) * NQF + q;
-    const double* op = up_s + ((e * 4 + f) * 5) * NQF + q;
-    double um[5], up[5];
+    // ---- face points: both traces at the owner's points; the flux needs the face max, so
+    //      each lane keeps its traces for its (at most FR) points between the two passes
+    constexpr int FR = (4 * NQF + 31) / 32;
+    double um[FR][5], up[FR][5];
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      um[c] = om[c * NQF];
-      up[c] = op[c * NQF];
-    }
-    auto nflux = [&](const double* w, double* fo) {
-      const double ri = 1.0 / w[0];
-      const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
-      const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
-      const double pd = p - A.pref;
-      fo[0] = w[0] * un;
-      fo[1] = fma(pd, nx, w[1] * un);
-      fo[2] = fma(pd, ny, w[2] * un);
-      fo[3] = fma(pd, nz, w[3] * un);
-      fo[4] = (w[4] + p) * un;
-    };
-    double fm[5], fp[5];
-    nflux(um, fm);
-    nflux(up, fp);
-    const double sc = G[3] * __ldg(T + M::O_WF + q);
+    for (int rr = 0; rr < FR; ++rr) {
+      const int fq = lane + 32 * rr;
+      if (fq >= 4 * NQF) break;
+      const int f = fq / NQF, q = fq - f * NQF;
+      const int code = A.code[size_t(k) * 4 + f], nb = A.nbr[size_t(k) * 4 + f];
+      const double* Gf = G + 9 + 4 * f;
+      int own_off = M::O_PSTD + f * NQF * NP, nb_off = 0;
+      if (code < CODE_GHOST) {
+        const int f2 = code / 6, sg = code - 6 * f2;
+        if (A.gid[k] < A.gid[nb]) {
+          nb_off = M::O_PMAP + ((f * 4 + f2) * 6 + sg) * NQF * NP;
+        } else {
+          own_off = M::O_PMAP + ((f2 * 4 + f) * 6 + PERM_INV[sg]) * NQF * NP;
+          nb_off = M::O_PSTD + f2 * NQF * NP;
+        }
+      }
+      if (q == 0) own_s[f] = own_off;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) om[c * NQF] = sc * (0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]));
-  }
-  __syncthreads();
-  // ---- projection onto the basis and the RK update (or rhs out); threads of a warp share (c, i)
-  double* r_s = up_s;
-  for (int idx = tid; idx < ne * 5 * NP; idx += NT) {
-    const int ci = idx / ne, e = idx - ci * ne, c = ci / NP, i = ci - c * NP;
-    double acc = 0;
+      for (int c = 0; c < 5; ++c) {
+        double acc = 0;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + own_off + q * NP + i), c_s[c * NP + i], acc);
+        um[rr][c] = acc;
+      }
+      if (code < CODE_GHOST) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double* D = T + M::O_DQ + (a * NP + i) * NQ;
-      const double* F = fv_s + e * FVS + (a * 5 + c) * NQ;
-      for (int q = 0; q < NQ; ++q) acc = fma(__ldg(D + q), F[q], acc);
+        for (int c = 0; c < 5; ++c) {
+          double acc = 0;
+          for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + nb_off + q * NP + i), cn_s[(f * 5 + c) * NP + i], acc);
+          up[rr][c] = acc;
+        }
+      } else {
+        ghost_trace(A, code - CODE_BC, um[rr], Gf[0], Gf[1], Gf[2], up[rr]);
+      }
+      auto speed = [&](const double (&w)[5]) {
+        const double ri = 1.0 / w[0];
+        const double un = (w[1] * Gf[0] + w[2] * Gf[1] + w[3] * Gf[2]) * ri;
+        const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+        return fabs(un) + sqrt(gamma * p * ri);
+      };
+      lam_s[fq] = fmax(speed(um[rr]), speed(up[rr]));
     }
-    for (int f = 0; f < 4; ++f) {
-      const double* Pt = T + own_s[e * 4 + f];
-      const double* F = um_s + ((e * 4 + f) * 5 + c) * NQF;
-      for (int q = 0; q < NQF; ++q) acc = fma(-__ldg(Pt + q * NP + i), F[q], acc);
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < FR; ++rr) {
+      const int fq = lane + 32 * rr;
+      if (fq >= 4 * NQF) break;
+      const int f = fq / NQF, q = fq - f * NQF;
+      const double* Gf = G + 9 + 4 * f;
+      const double nx = Gf[0], ny = Gf[1], nz = Gf[2];
+      double lam = lam_s[fq];
+      if (A.lambda_mode == 0)
+        for (int qq = 0; qq < NQF; ++qq) lam = fmax(lam, lam_s[f * NQF + qq]);
+      auto nflux = [&](const double (&w)[5], double* fo) {
+        const double ri = 1.0 / w[0];
+        const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
+        const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+        const double pd = p - A.pref;
+        fo[0] = w[0] * un;
+        fo[1] = fma(pd, nx, w[1] * un);
+        fo[2] = fma(pd, ny, w[2] * un);
+        fo[3] = fma(pd, nz, w[3] * un);
+        fo[4] = (w[4] + p) * un;
+      };
+      double fm[5], fp[5];
+      nflux(um[rr], fm);
+      nflux(up[rr], fp);
+      const double sc = Gf[3] * __ldg(T + M::O_WF + q);
+#pragma unroll
+      for (int c = 0; c < 5; ++c)
+        fs_s[c * 4 * NQF + fq] = sc * (0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[rr][c] - um[rr][c]));
     }
-    const int li = (e * 5 + c) * NP + i;
-    if (MODE == MODE_UPDATE) {
-      const size_t gi = size_t(e0) * 5 * NP + li;
-      const double rr = fma(A.a, A.res[gi], A.dt * acc);
-      A.res[gi] = rr;
-      A.Qout[gi] = fma(A.b, rr, c_s[li]);
-    } else {
-      r_s[li] = acc;
-    }
-  }
-  if (MODE == MODE_RHS) {   // public rhs as nodal values: V (dc/dt)
-    __syncthreads();
-    for (int idx = tid; idx < ne * 5 * NP; idx += NT) {
-      const int cn = idx / ne, e = idx - cn * ne, c = cn / NP, n = cn - c * NP;
+    __syncwarp();
+    // ---- projection onto the basis, update (or rhs out as nodal values)
+    constexpr int PR = (5 * NP + 31) / 32;
+    double rhs[PR];
+#pragma unroll
+    for (int rr = 0; rr < PR; ++rr) {
+      const int ci = lane + 32 * rr;
+      rhs[rr] = 0.0;
+      if (ci >= 5 * NP) break;
+      const int c = ci / NP, i = ci - c * NP;
       double acc = 0;
-      for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), r_s[(e * 5 + c) * NP + i], acc);
-      A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = acc;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double* D = T + M::O_DQ + (a * NP + i) * NQ;
+        const double* F = fv_s + (a * 5 + c) * NQ;
+        for (int q = 0; q < NQ; ++q) acc = fma(__ldg(D + q), F[q], acc);
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const double* Pt = T + own_s[f];
+        const double* F = fs_s + c * 4 * NQF + f * NQF;
+        for (int q = 0; q < NQF; ++q) acc = fma(-__ldg(Pt + q * NP + i), F[q], acc);
+      }
+      rhs[rr] = acc;
+      if (MODE == MODE_UPDATE) {
+        const size_t gi = size_t(k) * 5 * NP + ci;
+        const double r2 = fma(A.a, A.res[gi], A.dt * acc);
+        A.res[gi] = r2;
+        A.Qout[gi] = fma(A.b, r2, c_s[ci]);
+      }
     }
+    if (MODE == MODE_RHS) {   // V (dc/dt) into the public layout, staged in the flux buffer
+      __syncwarp();
+#pragma unroll
+      for (int rr = 0; rr < PR; ++rr) {
+        const int ci = lane + 32 * rr;
+        if (ci < 5 * NP) fv_s[ci] = rhs[rr];
+      }
+      __syncwarp();
+      for (int cn = lane; cn < 5 * NP; cn += 32) {
+        const int c = cn / NP, n = cn - c * NP;
+        double acc = 0;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), fv_s[c * NP + i], acc);
+        A.out[(size_t(c) * A.Kpub + A.pub[k]) * NP + n] = acc;
+      }
+    }
+    __syncwarp();   // the warp's slice is reused by its next element
   }
 }
 
