@@ -279,6 +279,9 @@ dg_status dg_mesh_create(const dg_mesh_desc* desc, int rank, dg_ctx** out) {
 
 void dg_destroy(dg_ctx* c) {
   if (!c) return;
+  for (void*& g : c->graph_exec)
+    if (g) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
+  if (c->capture_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->capture_stream));
   if (c->comm) ncclCommDestroy(static_cast<ncclComm_t>(c->comm));
   if (c->comm_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->comm_stream));
   if (c->ev_packed) cudaEventDestroy(static_cast<cudaEvent_t>(c->ev_packed));
@@ -359,6 +362,11 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   c->dscratch = reinterpret_cast<double*>(take(4096 * 8));
   c->dsw = reinterpret_cast<double*>(take(size_t(DG_MAX_SENSORS) * c->Np * 8));
   c->dsel = reinterpret_cast<int32_t*>(take(size_t(DG_MAX_SENSORS) * 4));
+  for (void*& g : c->graph_exec)   // captured steps point into the previous workspace
+    if (g) {
+      cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
+      g = nullptr;
+    }
   c->rec_buf = nullptr;
   c->ws = dptr;
   c->ws_bytes = nbytes;
@@ -533,7 +541,67 @@ dg_status dg_rk_step(dg_ctx* c, double dt, int nsteps, void* stream) {
   if (nsteps < 0 || !std::isfinite(dt)) return set_err(c, DG_EARG, "bad dt or nsteps");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool multi = c->nparts > 1 && !c->peers.empty();
-  for (int n = 0; n < nsteps; ++n) {
+  // single partition, no time-dependent boundary, no per-step host work: replay one captured
+  // step (its stage launches) as a CUDA graph; the first step of a new dt runs eagerly
+  const bool graphable = !multi && !c->has_inflow && !c->rec_buf && c->check_every == 0 &&
+                         std::getenv("DG_NO_GRAPHS") == nullptr;
+  if (graphable && c->graph_dt != dt) {
+    for (void*& g : c->graph_exec)
+      if (g) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
+        g = nullptr;
+      }
+    c->graph_dt = dt;
+  }
+  int n = 0;
+  if (graphable && nsteps > 1) {
+    if (!c->graph_exec[0] && !c->graph_exec[1]) {   // eager first step: sets kernel attributes
+      for (int s = 0; s < nstages(c); ++s) {
+        dg_status e = compute_stage(c, s, dt, 3, st);
+        if (e) return e;
+        dg_stage_finish(c, s, dt);
+      }
+      n = 1;
+    }
+    for (; n < nsteps; ++n) {
+      cudaGraphExec_t& ex = reinterpret_cast<cudaGraphExec_t&>(c->graph_exec[c->cur]);
+      if (!ex) {
+        if (!c->capture_stream) {
+          cudaStream_t cs;
+          CUDA_TRY(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+          c->capture_stream = cs;
+        }
+        cudaStream_t cs = static_cast<cudaStream_t>(c->capture_stream);
+        const int cur0 = c->cur;
+        const double t0 = c->t;
+        const int64_t l0 = c->launches, s0n = c->steps_done;
+        CUDA_TRY(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int s = 0; s < nstages(c); ++s) {
+          dg_status e = compute_stage(c, s, dt, 3, cs);
+          if (e) {
+            cudaGraph_t gbad = nullptr;
+            cudaStreamEndCapture(cs, &gbad);
+            if (gbad) cudaGraphDestroy(gbad);
+            return e;
+          }
+          dg_stage_finish(c, s, dt);
+        }
+        cudaGraph_t gr;
+        CUDA_TRY(c, cudaStreamEndCapture(cs, &gr));
+        CUDA_TRY(c, cudaGraphInstantiate(&ex, gr, 0));
+        cudaGraphDestroy(gr);
+        c->cur = cur0;   // capturing ran nothing: restore the step state
+        c->t = t0;
+        c->steps_done = s0n;
+        c->launches = l0;
+      }
+      CUDA_TRY(c, cudaGraphLaunch(ex, st));
+      for (int s = 0; s < nstages(c); ++s) dg_stage_finish(c, s, dt);
+      c->launches += nstages(c);
+    }
+    return DG_OK;
+  }
+  for (; n < nsteps; ++n) {
     for (int s = 0; s < nstages(c); ++s) {
       if (multi) {
         dg_status e = halo_exchange(c, st);

@@ -84,6 +84,12 @@ struct dg_ctx {
   int64_t launches = 0;
   std::string err;
 
+  // ---- CUDA graphs of one RK step (single partition): [start buffer cur] for the cached dt
+  void* graph_exec[2] = {nullptr, nullptr};
+  void* capture_stream = nullptr;
+  double graph_dt = 0.0;
+  bool has_inflow = false;
+
   // ---- NCCL (opaque to keep nccl.h out of the host translation units)
   void* comm = nullptr;
   void* comm_stream = nullptr;

@@ -177,6 +177,8 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   // geo: 25 doubles, code: 4 bytes per element); the few interior elements moved into the
   // boundary range merely wait for the halo
   c->K_int = int64_t(inter.size()) / 32 * 32;
+  for (int64_t k : mine)
+    for (int f = 0; f < 4; ++f) c->has_inflow |= d->bc[4 * k + f] == DG_BC_INFLOW;
   c->gid = inter;
   c->gid.insert(c->gid.end(), bound.begin(), bound.end());
   std::vector<int64_t> g2l(K, -1), g2pub(K, -1);
