@@ -334,7 +334,11 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
 
 template <int N>
 struct WS {
+#ifdef DG_WS_EB
+  static constexpr int EB = DG_WS_EB;
+#else
   static constexpr int EB = (N <= 2) ? 32 : 16;
+#endif
   // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 3 the
   // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3)
 #ifdef DG_WS_PW
@@ -392,7 +396,7 @@ struct WS {
 };
 
 #ifndef DG_KUNROLL
-#define DG_KUNROLL 4
+#define DG_KUNROLL 6
 #endif
 constexpr int KUNROLL = DG_KUNROLL;   // consumer k-loop unroll (register pressure vs load hoisting)
 
