@@ -859,7 +859,16 @@ struct HO {
   static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
   static constexpr int GS = HS ? S::NP - 8 * (S::NTL - 1) : 0;
   static constexpr int OPW = NPG * 64 + 4 * GS;                   // doubles per k-step of Op
+#ifdef DG_HO_KC
+  static constexpr int KC = DG_HO_KC;
+#else
   static constexpr int KC = (N == 6) ? 6 : 7;                     // k-steps per ring chunk
+#endif
+#ifdef DG_HO_SLOTS
+  static constexpr int NSLOT = DG_HO_SLOTS;
+#else
+  static constexpr int NSLOT = 3;                                 // ring slots
+#endif
   static constexpr int NCH = (S::KS4 + KC - 1) / KC;
   static constexpr int KLAST = S::KS4 - (NCH - 1) * KC;          // k-steps of the last chunk
   static constexpr uint32_t BCH = uint32_t(KC) * OPW * 8;
@@ -876,7 +885,7 @@ struct HO {
   static constexpr size_t SMEM_X = size_t(ROWS) * XS * 8;
   static_assert(2 * size_t(BQ) <= SMEM_X, "X doubles as the output staging tile");
   static constexpr size_t SMEM_T = size_t(2 * 96 * S::NFP + 4 * S::NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = SMEM_X + 2 * size_t(BIN) + 3 * size_t(BCH) + SMEM_T + 64;
+  static constexpr size_t SMEM = SMEM_X + 2 * size_t(BIN) + NSLOT * size_t(BCH) + SMEM_T + 16 * (2 + 2 * NSLOT);
   static_assert(SMEM <= 227 * 1024, "high-order tile does not fit in shared memory");
 };
 
@@ -948,10 +957,10 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
   double* sX = reinterpret_cast<double*>(smem);
   unsigned char* in0 = smem + H::SMEM_X;
   double* ring = reinterpret_cast<double*>(in0 + 2 * H::BIN);
-  uint8_t* sTbl = reinterpret_cast<uint8_t*>(ring) + 3 * H::BCH;
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(ring) + H::NSLOT * H::BCH;
   uint8_t* sTblf = sTbl + 96 * NFP;
   uint8_t* sFm = sTblf + 96 * NFP;
-  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + H::SMEM_T);   // [0,1] inputs, [2..4] full, [5..7] empty
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + H::SMEM_T);   // [0,1] inputs, then ring full, ring empty
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   auto bufQ = [&](int b) { return reinterpret_cast<double*>(in0 + b * H::BIN); };
   auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * H::BIN + H::BQ); };
@@ -965,8 +974,8 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
   for (int i = tid; i < 4 * NFP; i += NT) sFm[i] = A.fmask[i];
   for (int i = tid; i < H::ROWS * XS; i += NT) sX[i] = 0.0;   // padding columns stay 0
   if (tid == 0) {
-    for (int b = 0; b < 5; ++b) mbar_init(&sBar[b], 1);
-    for (int b = 5; b < 8; ++b) mbar_init(&sBar[b], H::NW);
+    for (int b = 0; b < 2 + H::NSLOT; ++b) mbar_init(&sBar[b], 1);                    // inputs, ring full
+    for (int b = 2 + H::NSLOT; b < 2 + 2 * H::NSLOT; ++b) mbar_init(&sBar[b], H::NW);  // ring empty
   }
   __syncthreads();
 
@@ -985,7 +994,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     tma_load_1d(bufC(b), A.code + size_t(e0) * 4, H::BC, &sBar[b]);
   };
   auto load_chunk = [&](long long gc) {   // one thread; the slot is free
-    const int s = int(gc % 3), c = int(gc % H::NCH);
+    const int s = int(gc % H::NSLOT), c = int(gc % H::NCH);
     const int kc = min(H::KC, S::KS4 - c * H::KC);
     const uint32_t bytes = uint32_t(kc) * H::OPW * 8;
     mbar_arrive_expect_tx(&sBar[2 + s], bytes);
@@ -996,7 +1005,8 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     // have released it
     if (lane == 0)
       for (long long gn = 0; gn < nchunks; ++gn) {
-        if (gn >= 3) mbar_wait(&sBar[5 + int(gn % 3)], uint32_t(((gn / 3) - 1) & 1));
+        if (gn >= H::NSLOT)
+          mbar_wait(&sBar[2 + H::NSLOT + int(gn % H::NSLOT)], uint32_t(((gn / H::NSLOT) - 1) & 1));
         load_chunk(gn);
       }
     return;
@@ -1176,11 +1186,11 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
 #endif
     for (int c = 0; c < H::NCH; ++c) {
       const long long gc = gch + c;
-      const int s = int(gc % 3);
+      const int s = int(gc % H::NSLOT);
 #if DG_TRACE
       long long tw0 = clock64();
 #endif
-      mbar_wait(&sBar[2 + s], uint32_t((gc / 3) & 1));
+      mbar_wait(&sBar[2 + s], uint32_t((gc / H::NSLOT) & 1));
 #if DG_TRACE
       wfull += clock64() - tw0;
 #endif
@@ -1204,7 +1214,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         else run(std::integral_constant<int, H::KLAST>{});
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sBar[5 + s]);
+      if (lane == 0) mbar_arrive(&sBar[2 + H::NSLOT + s]);
       __syncwarp();
     }
     gch += H::NCH;
