@@ -146,7 +146,7 @@ cudaError_t launch_modal_p(const dgk::StageArgs& A, cudaStream_t st) {
   }
   const int nel = A.e_end - A.e_begin;
   if (nel <= 0) return cudaSuccess;
-  const int grid = std::min((nel + W::WPC - 1) / W::WPC, 8 * num_sms());
+  const int grid = std::min((nel + W::WPC * W::EPW - 1) / (W::WPC * W::EPW), 8 * num_sms());
   dgk::modal_warp_kernel<P, MODE><<<grid, W::NT, W::SMEM, st>>>(A);
   return cudaGetLastError();
 }

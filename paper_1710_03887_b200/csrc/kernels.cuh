@@ -1302,43 +1302,55 @@ template <int P>
 struct MW {
   using M = MS<P>;
   static constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF;
+  static constexpr int EPW = NQ <= 8 ? 4 : 1;                          // elements per warp
   static constexpr int WPC = P <= 2 ? 8 : 4, NT = 32 * WPC;           // warps per CTA
-  static constexpr int MINB = P == 1 ? 4 : P == 2 ? 2 : 1;             // CTAs per SM (register cap)
-  static constexpr int W_C = 0, W_CN = W_C + 5 * NP, W_FV = W_CN + 4 * 5 * NP, W_LAM = W_FV + 15 * NQ,
-                       W_FS = W_LAM + 4 * NQF, W_END = W_FS + 5 * 4 * NQF;
-  static constexpr int WSTRIDE = W_END + 1;                            // doubles per warp (odd)
-  static constexpr size_t SMEM = size_t(WPC) * WSTRIDE * 8 + size_t(WPC) * 4 * 4;
+  static constexpr int MINB = P <= 2 ? 2 : 1;                          // CTAs per SM (register cap)
+  // one element's slice: coefficients, neighbours' coefficients, volume fluxes, wave speeds,
+  // weighted face fluxes
+  static constexpr int E_C = 0, E_CN = E_C + 5 * NP, E_FV = E_CN + 4 * 5 * NP, E_LAM = E_FV + 15 * NQ,
+                       E_FS = E_LAM + 4 * NQF, E_END = E_FS + 5 * 4 * NQF;
+  static constexpr int ESTRIDE = E_END | 1;                            // odd: element-parallel reads
+  static constexpr int WSTRIDE = EPW * ESTRIDE;
+  static constexpr size_t SMEM = size_t(WPC) * WSTRIDE * 8 + size_t(WPC) * EPW * 4 * 4;
 };
 
+// Each warp owns EPW elements at a time (persistent CTAs, warps stride over element groups),
+// their coefficients, their neighbours' coefficients and their quadrature values in a private
+// slice of shared memory; lanes map to (element, quadrature point) for the interpolations and
+// fluxes and to (element, field, mode) for the projections; only __syncwarp between steps.
 template <int P, int MODE>
 __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(const StageArgs A) {
   using M = MS<P>;
   using W = MW<P>;
-  constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF;
+  constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF, EPW = W::EPW, ES = W::ESTRIDE;
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* ws = sm + warp * W::WSTRIDE;
-  double* c_s = ws + W::W_C;      // [5][NP]
-  double* cn_s = ws + W::W_CN;    // [4][5][NP]
-  double* fv_s = ws + W::W_FV;    // [3][5][NQ]
-  double* lam_s = ws + W::W_LAM;  // [4][NQF]
-  double* fs_s = ws + W::W_FS;    // [5][4][NQF]  Fscale w F*
-  int* own_s = reinterpret_cast<int*>(sm + W::WPC * W::WSTRIDE) + warp * 4;
+  int* own_s = reinterpret_cast<int*>(sm + W::WPC * W::WSTRIDE) + warp * EPW * 4;   // [EPW][4]
   const double* T = A.op;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
   const int nel = A.e_end - A.e_begin;
-  for (int el = blockIdx.x * W::WPC + warp; el < nel; el += gridDim.x * W::WPC) {
-    const int k = A.e_begin + el;
-    const double* G = A.geo + size_t(k) * GEO;
-    for (int i = lane; i < 5 * NP; i += 32) c_s[i] = A.Qin[size_t(k) * 5 * NP + i];
-    for (int i = lane; i < 4 * 5 * NP; i += 32) {
-      const int f = i / (5 * NP), r0 = i - f * 5 * NP;
+  for (int g0 = (blockIdx.x * W::WPC + warp) * EPW; g0 < nel; g0 += gridDim.x * W::WPC * EPW) {
+    const int ne = min(EPW, nel - g0);
+    const int k0 = A.e_begin + g0;
+    for (int i = lane; i < ne * 5 * NP; i += 32) {
+      const int ee = i / (5 * NP), r0 = i - ee * 5 * NP;
+      ws[ee * ES + W::E_C + r0] = A.Qin[size_t(k0 + ee) * 5 * NP + r0];
+    }
+    for (int i = lane; i < ne * 4 * 5 * NP; i += 32) {
+      const int ee = i / (20 * NP), r1 = i - ee * 20 * NP, f = r1 / (5 * NP), r0 = r1 - f * 5 * NP;
+      const int k = k0 + ee;
       const int code = A.code[size_t(k) * 4 + f];
-      cn_s[i] = code < CODE_GHOST ? __ldg(A.Qin + size_t(A.nbr[size_t(k) * 4 + f]) * 5 * NP + r0) : 0.0;
+      ws[ee * ES + W::E_CN + r1] =
+          code < CODE_GHOST ? __ldg(A.Qin + size_t(A.nbr[size_t(k) * 4 + f]) * 5 * NP + r0) : 0.0;
     }
     __syncwarp();
     // ---- volume points: values, validity, contravariant fluxes
-    for (int q = lane; q < NQ; q += 32) {
+    for (int v = lane; v < ne * NQ; v += 32) {
+      const int ee = v / NQ, q = v - ee * NQ;
+      const int k = k0 + ee;
+      const double* c_s = ws + ee * ES + W::E_C;
+      const double* G = A.geo + size_t(k) * GEO;
       double u[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
@@ -1351,6 +1363,7 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
       const double p = gm1 * (u[4] - 0.5 * (u[1] * vx + u[2] * vy + u[3] * vz));
       if (!state_ok(u[0], p, u[1], u[2], u[3], u[4])) flag_blowup(A.flag, A.gid[k]);
       const double pd = p - A.pref, Ep = u[4] + p;
+      double* fv_s = ws + ee * ES + W::E_FV;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double cx = G[3 * a], cy = G[3 * a + 1], cz = G[3 * a + 2];
@@ -1363,17 +1376,20 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
         o[4 * NQ] = Ep * U;
       }
     }
-    // ---- face points: both traces at the owner's points; the flux needs the face max, so
-    //      each lane keeps its traces for its (at most FR) points between the two passes
-    constexpr int FR = (4 * NQF + 31) / 32;
+    // ---- face points: both traces at the owner's points; each lane keeps the traces of its
+    //      (at most FR) points for the flux pass after the face max
+    constexpr int FR = (EPW * 4 * NQF + 31) / 32;
     double um[FR][5], up[FR][5];
 #pragma unroll
     for (int rr = 0; rr < FR; ++rr) {
-      const int fq = lane + 32 * rr;
-      if (fq >= 4 * NQF) break;
-      const int f = fq / NQF, q = fq - f * NQF;
+      const int v = lane + 32 * rr;
+      if (v >= ne * 4 * NQF) break;
+      const int ee = v / (4 * NQF), fq = v - ee * 4 * NQF, f = fq / NQF, q = fq - f * NQF;
+      const int k = k0 + ee;
+      const double* c_s = ws + ee * ES + W::E_C;
+      const double* cn_s = ws + ee * ES + W::E_CN;
       const int code = A.code[size_t(k) * 4 + f], nb = A.nbr[size_t(k) * 4 + f];
-      const double* Gf = G + 9 + 4 * f;
+      const double* Gf = A.geo + size_t(k) * GEO + 9 + 4 * f;
       int own_off = M::O_PSTD + f * NQF * NP, nb_off = 0;
       if (code < CODE_GHOST) {
         const int f2 = code / 6, sg = code - 6 * f2;
@@ -1384,7 +1400,7 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
           nb_off = M::O_PSTD + f2 * NQF * NP;
         }
       }
-      if (q == 0) own_s[f] = own_off;
+      if (q == 0) own_s[ee * 4 + f] = own_off;
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         double acc = 0;
@@ -1407,16 +1423,17 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
         const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
         return fabs(un) + sqrt(gamma * p * ri);
       };
-      lam_s[fq] = fmax(speed(um[rr]), speed(up[rr]));
+      ws[ee * ES + W::E_LAM + fq] = fmax(speed(um[rr]), speed(up[rr]));
     }
     __syncwarp();
 #pragma unroll
     for (int rr = 0; rr < FR; ++rr) {
-      const int fq = lane + 32 * rr;
-      if (fq >= 4 * NQF) break;
-      const int f = fq / NQF, q = fq - f * NQF;
-      const double* Gf = G + 9 + 4 * f;
+      const int v = lane + 32 * rr;
+      if (v >= ne * 4 * NQF) break;
+      const int ee = v / (4 * NQF), fq = v - ee * 4 * NQF, f = fq / NQF, q = fq - f * NQF;
+      const double* Gf = A.geo + size_t(k0 + ee) * GEO + 9 + 4 * f;
       const double nx = Gf[0], ny = Gf[1], nz = Gf[2];
+      const double* lam_s = ws + ee * ES + W::E_LAM;
       double lam = lam_s[fq];
       if (A.lambda_mode == 0)
         for (int qq = 0; qq < NQF; ++qq) lam = fmax(lam, lam_s[f * NQF + qq]);
@@ -1435,20 +1452,24 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
       nflux(um[rr], fm);
       nflux(up[rr], fp);
       const double sc = Gf[3] * __ldg(T + M::O_WF + q);
+      double* fs_s = ws + ee * ES + W::E_FS;
 #pragma unroll
       for (int c = 0; c < 5; ++c)
         fs_s[c * 4 * NQF + fq] = sc * (0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[rr][c] - um[rr][c]));
     }
     __syncwarp();
     // ---- projection onto the basis, update (or rhs out as nodal values)
-    constexpr int PR = (5 * NP + 31) / 32;
+    constexpr int PR = (EPW * 5 * NP + 31) / 32;
     double rhs[PR];
 #pragma unroll
     for (int rr = 0; rr < PR; ++rr) {
-      const int ci = lane + 32 * rr;
+      const int v = lane + 32 * rr;
       rhs[rr] = 0.0;
-      if (ci >= 5 * NP) break;
-      const int c = ci / NP, i = ci - c * NP;
+      if (v >= ne * 5 * NP) break;
+      const int ee = v / (5 * NP), ci = v - ee * 5 * NP, c = ci / NP, i = ci - c * NP;
+      const int k = k0 + ee;
+      const double* fv_s = ws + ee * ES + W::E_FV;
+      const double* fs_s = ws + ee * ES + W::E_FS;
       double acc = 0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -1458,7 +1479,7 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
       }
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
-        const double* Pt = T + own_s[f];
+        const double* Pt = T + own_s[ee * 4 + f];
         const double* F = fs_s + c * 4 * NQF + f * NQF;
         for (int q = 0; q < NQF; ++q) acc = fma(-__ldg(Pt + q * NP + i), F[q], acc);
       }
@@ -1467,25 +1488,29 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
         const size_t gi = size_t(k) * 5 * NP + ci;
         const double r2 = fma(A.a, A.res[gi], A.dt * acc);
         A.res[gi] = r2;
-        A.Qout[gi] = fma(A.b, r2, c_s[ci]);
+        A.Qout[gi] = fma(A.b, r2, ws[ee * ES + W::E_C + ci]);
       }
     }
-    if (MODE == MODE_RHS) {   // V (dc/dt) into the public layout, staged in the flux buffer
+    if (MODE == MODE_RHS) {   // V (dc/dt) into the public layout, staged in the volume-flux slice
       __syncwarp();
 #pragma unroll
       for (int rr = 0; rr < PR; ++rr) {
-        const int ci = lane + 32 * rr;
-        if (ci < 5 * NP) fv_s[ci] = rhs[rr];
+        const int v = lane + 32 * rr;
+        if (v < ne * 5 * NP) {
+          const int ee = v / (5 * NP), ci = v - ee * 5 * NP;
+          ws[ee * ES + W::E_FV + ci] = rhs[rr];
+        }
       }
       __syncwarp();
-      for (int cn = lane; cn < 5 * NP; cn += 32) {
-        const int c = cn / NP, n = cn - c * NP;
+      for (int v = lane; v < ne * 5 * NP; v += 32) {
+        const int ee = v / (5 * NP), cn = v - ee * 5 * NP, c = cn / NP, n = cn - c * NP;
+        const double* r_s = ws + ee * ES + W::E_FV;
         double acc = 0;
-        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), fv_s[c * NP + i], acc);
-        A.out[(size_t(c) * A.Kpub + A.pub[k]) * NP + n] = acc;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), r_s[c * NP + i], acc);
+        A.out[(size_t(c) * A.Kpub + A.pub[k0 + ee]) * NP + n] = acc;
       }
     }
-    __syncwarp();   // the warp's slice is reused by its next element
+    __syncwarp();   // the warp's slice is reused by its next element group
   }
 }
 
