@@ -409,6 +409,7 @@ struct ConsumerIO {
   unsigned char* in0;
   double* sRes;
   uint64_t* barRes;
+  uint64_t* barIn;
   int nmine, ctid, lane;
 };
 
@@ -487,6 +488,19 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     mbar_arrive_expect_tx(io.barRes + jj % W::NRES, W::BQ);
     tma_load_1d(res_buf(jj), A.res + size_t(e0) * 5 * NP, W::BQ, io.barRes + jj % W::NRES);
   };
+  // with two input buffers the consumer that releases a buffer (its Q bulk store has been read)
+  // refills it with the inputs of the tile two ahead, so the producers never wait for it
+  auto fetch_in = [&](int jj) {   // one thread, full tiles only
+    const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
+    const int b = jj % W::NIN;
+    unsigned char* ib = io.in0 + b * W::BIN;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(io.barIn + b, W::BIN);
+    tma_load_1d(ib, A.Qin + size_t(e0) * 5 * NP, W::BQ, io.barIn + b);
+    tma_load_1d(ib + W::BQ, A.geo + size_t(e0) * GEO, W::BG, io.barIn + b);
+    tma_load_1d(ib + W::BQ + W::BG, A.nbr + size_t(e0) * 4, W::BN, io.barIn + b);
+    tma_load_1d(ib + W::BQ + W::BG + W::BN, A.code + size_t(e0) * 4, W::BC, io.barIn + b);
+  };
   if (MODE == MODE_UPDATE && io.ctid == 0 && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
@@ -550,14 +564,15 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 0);
     nbar_sync(W::BAR_XV_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 1);
+    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
+      // tile j-1's residual store has left sRes by now (issued at the end of its epilogue)
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      load_res(j);
+    }
     kloop(KBlk<XSV, 0, S::KSV>{});
     if (io.ctid < 32) trace_ev(A, j, 2);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
 
-    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // res(j-1) left sRes
-      load_res(j);
-    }
     nbar_sync(W::BAR_XF_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 3);
     kloop(KBlk<XSF, S::KSV, S::KS4>{});
@@ -651,9 +666,18 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       }
     }
     if (io.ctid < 32) trace_ev(A, j, 5);
-    // only consumer warp 0 signals the Q buffer free (after BAR_C and its lane 0 saw the Q
-    // bulk read finish)
-    if (j + W::NIN < io.nmine && io.ctid < 32) {
+    if (W::NIN == 2) {
+      // full tiles: this thread refills the buffer (its Q store has been read, or, without a
+      // store, nobody reads it any more); the partial last tile is loaded by the producers,
+      // who wait for consumer warp 0 to signal the buffer free
+      if (io.ctid == 0 && j + 2 < io.nmine && tile_full(j + 2)) fetch_in(j + 2);
+      if (j + 2 < io.nmine && !tile_full(j + 2) && io.ctid < 32) {
+        __syncwarp();
+        nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
+      }
+    } else if (j + W::NIN < io.nmine && io.ctid < 32) {
+      // only consumer warp 0 signals the Q buffer free (after BAR_C and its lane 0 saw the Q
+      // bulk read finish)
       __syncwarp();
       nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
     }
@@ -736,6 +760,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       }
     };
     if (nmine > 0) fetch(0);
+    if (W::NIN == 2 && nmine > 1) fetch(1);   // later full tiles are fetched by the consumers
     for (int j = 0; j < nmine; ++j) {
       const int tile = blockIdx.x + j * gridDim.x;
       const int e0 = A.e_begin + tile * EB;
@@ -803,7 +828,12 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       nbar_arrive(W::BAR_XV_FULL, NT);
       // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1;
       //      the Q_EMPTY sync also covers every producer thread having left tile j-1)
-      if (j + 1 < nmine) {
+      if (W::NIN == 2) {
+        if (j + 1 < nmine && j + 1 >= 2 && A.e_end - (A.e_begin + (int(blockIdx.x) + (j + 1) * int(gridDim.x)) * EB) < EB) {
+          nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);   // the partial last tile
+          fetch(j + 1);
+        }
+      } else if (j + 1 < nmine) {
         if (j + 1 >= W::NIN) nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
         fetch(j + 1);
       }
@@ -821,7 +851,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     // without run-time branches
     using PL = M8Plan<N>;
     const int cw = warp;
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], nmine, tid, lane};
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
