@@ -515,7 +515,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     // the odd n-tile has only GS real columns: with GS <= 4 it is cheaper on DFMA (GS per k-step
     // and lane, partial sums over the lane's k = t mod 4, reduced by two shuffles) than as a
     // full 8-column DMMA (16 pipe cycles for GS useful columns)
-    constexpr bool SDF = W::GS > 0 && W::GS <= 4;
+#ifndef DG_SDF
+#define DG_SDF 1
+#endif
+    constexpr bool SDF = DG_SDF && W::GS > 0 && W::GS <= 4;
     double sacc[NSING > 0 ? NSING : 1][4];
 #pragma unroll
     for (int k = 0; k < NSING; ++k) sacc[k][0] = sacc[k][1] = sacc[k][2] = sacc[k][3] = 0.0;
