@@ -134,9 +134,27 @@ __device__ __forceinline__ void inflow_state(double t, double alpha, double gamm
 
 enum { MODE_UPDATE = 0, MODE_RHS = 1 };
 
-// Reciprocal and square root from the MUFU seeds plus two Newton steps each: within
-// ~1 ulp of the correctly rounded results (the parity tests bound the effect), at a
-// third of the issue cost of IEEE div/sqrt with their slow-path branches.
+// Reciprocal and square root from the MUFU seeds plus one third-order correction each
+// (seed error e -> O(e^3), below 1 ulp for the ~2^-20 seeds): within ~1 ulp of the
+// correctly rounded results (the parity tests bound the effect), at a fraction of the
+// issue cost of IEEE div/sqrt with their slow-path branches.
+//   1/x:     e = 1 - x y,   y' = y (1 + e + e^2)                  (x y' = 1 - e^3)
+//   sqrt(x): d = 1 - x y^2, sqrt(x) = x y (1 - d)^(-1/2) = x y (1 + d/2 + 3 d^2/8 + O(d^3))
+#ifndef DG_NEWTON2
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+}
+__device__ __forceinline__ double sqrt_nr(double x) {   // x > 0
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
+  const double xy = x * y;
+  const double d = fma(-xy, y, 1.0);
+  return fma(xy, d * fma(0.375, d, 0.5), xy);
+}
+#else   // two Newton steps each (the previous form; experiment knob)
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
@@ -154,6 +172,7 @@ __device__ __forceinline__ double sqrt_nr(double x) {   // x > 0
   y = fma(0.5 * y, e, y);
   return x * y;
 }
+#endif
 
 // Neighbour trace for a paired face (local element or halo record); boundary faces are filled later.
 template <int NP, int NFP>
