@@ -414,10 +414,16 @@ struct WS {
                        BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9;
 };
 
-#ifndef DG_KUNROLL
-#define DG_KUNROLL 6
+// consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
+// (C4 55.1 vs 54.9 GDOF/s at 6), 6 at N <= 3; DG_KUNROLL overrides for experiments
+template <int N>
+constexpr int kunroll() {
+#ifdef DG_KUNROLL
+  return DG_KUNROLL;
+#else
+  return N == 4 ? 7 : 6;
 #endif
-constexpr int KUNROLL = DG_KUNROLL;   // consumer k-loop unroll (register pressure vs load hoisting)
+}
 
 template <int N, int MODE>
 struct ConsumerIO {
@@ -553,7 +559,8 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
       if (A.debug & 1) return;
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
-#pragma unroll KUNROLL
+      constexpr int KU = kunroll<N>();
+#pragma unroll KU
       for (int ks = K0; ks < K1; ++ks) {
         const double* ob = io.sOp + ks * W::OPW;
 #pragma unroll

@@ -121,7 +121,10 @@ def test_orientation_repair_and_errors():
     with pytest.raises(dg.DGError) as e:
         dg.dg_mesh_create(1, flat, np.array([[0, 1, 2, 3]]), np.full((1, 4), 1))
     assert e.value.status == dg.DG_EMESH
-    # bad arguments
+    # bad arguments (an empty mesh included)
+    with pytest.raises(dg.DGError) as e:
+        dg.dg_mesh_create(2, np.zeros((0, 3)), np.zeros((0, 4), dtype=np.int64), np.zeros((0, 4), dtype=np.int32))
+    assert e.value.status == dg.DG_EARG
     with pytest.raises(dg.DGError) as e:
         dg.dg_mesh_create(0, m.vxyz, m.etov, m.bc)
     assert e.value.status == dg.DG_EARG
