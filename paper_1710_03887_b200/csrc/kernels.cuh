@@ -918,6 +918,10 @@ struct HO {
   static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
   static constexpr int GS = HS ? S::NP - 8 * (S::NTL - 1) : 0;
   static constexpr int OPW = NPG * 64 + 4 * GS;                   // doubles per k-step of Op
+#ifndef DG_HO_SDF
+#define DG_HO_SDF 1
+#endif
+  static constexpr bool SDF = DG_HO_SDF && GS > 0 && GS <= 4;     // odd n-tile on DFMA (N = 6)
 #ifdef DG_HO_KC
   static constexpr int KC = DG_HO_KC;
 #else
@@ -994,6 +998,18 @@ __device__ __forceinline__ void ho_chunk(double (&acc)[HO<N>::MU][2][2], const d
         const double a = xa[m * 8 * H::XS + kcol];
         dmma_8x8x4(acc[m][0], a, b.x);
         dmma_8x8x4(acc[m][1], a, b.y);
+      }
+    } else if (H::SDF) {
+      // odd n-tile with GS <= 4 real columns on DFMA: lane (g, t) accumulates row g x column c
+      // over its k = t (mod 4) in acc[m][c / 2][c % 2]; reduced over t after the contraction
+      double bv[H::GS];
+#pragma unroll
+      for (int c = 0; c < H::GS; ++c) bv[c] = ob[kk * H::OPW + 4 * c + (lane & 3)];
+#pragma unroll
+      for (int m = 0; m < MC; ++m) {
+        const double a = xa[m * 8 * H::XS + kcol];
+#pragma unroll
+        for (int c = 0; c < H::GS; ++c) acc[m][c >> 1][c & 1] = fma(a, bv[c], acc[m][c >> 1][c & 1]);
       }
     } else {
       const double b = lane < 4 * H::GS ? ob[kk * H::OPW + lane] : 0.0;
@@ -1277,6 +1293,23 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       __syncwarp();
     }
     gch += H::NCH;
+    if (H::SDF && it.kind == 1) {
+      // sum the DFMA partials over the 4 lanes of a row; lanes t = 0, 1 take columns 2t, 2t+1
+      // (the DMMA accumulator layout the epilogue expects)
+#pragma unroll
+      for (int m = 0; m < MU; ++m) {
+        double sv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double v = c < H::GS ? acc[m][c >> 1][c & 1] : 0.0;
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          sv[c] = v;
+        }
+        acc[m][0][0] = t4 == 0 ? sv[0] : t4 == 1 ? sv[2] : 0.0;
+        acc[m][0][1] = t4 == 0 ? sv[1] : t4 == 1 ? sv[3] : 0.0;
+      }
+    }
     if (warp == 0) trace_ev(A, j, 7);
 #if DG_TRACE
     if (tid == 0 && blockIdx.x == 0 && j < 64 && A.trace) {
