@@ -502,6 +502,15 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #pragma unroll
   for (int k = 0; k < NSING; ++k) mts[k] = singles[k];
   constexpr int NSLOT = 2 * NPAIR + NSING;
+  // the consumer warp whose lane 0 issues the tile's TMA traffic (residual load, input refill,
+  // bulk stores) and waits for the bulk-store reads: the last one (fewest pair units; measured
+  // C4 55.0 vs 54.9, C3 55.0 vs 54.8 GDOF/s with warp 0)
+#ifdef DG_WS_IOW
+  constexpr int IOW = DG_WS_IOW < W::CW ? DG_WS_IOW : 0;
+#else
+  constexpr int IOW = W::CW - 1;
+#endif
+  constexpr int IOT = 32 * IOW;
   auto tile_full = [&](int jj) {
     const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
     return A.e_end - e0 >= EB;
@@ -526,7 +535,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     tma_load_1d(ib + W::BQ + W::BG, A.nbr + size_t(e0) * 4, W::BN, io.barIn + b);
     tma_load_1d(ib + W::BQ + W::BG + W::BN, A.code + size_t(e0) * 4, W::BC, io.barIn + b);
   };
-  if (MODE == MODE_UPDATE && io.ctid == 0 && io.nmine > 0 && tile_full(0)) load_res(0);
+  if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     const int e0 = A.e_begin + tile * EB;
@@ -593,7 +602,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 0);
     nbar_sync(W::BAR_XV_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 1);
-    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == 0 && j >= 1 && ne == EB) {
+    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
       // tile j-1's residual store has left sRes by now (issued at the end of its epilogue)
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       load_res(j);
@@ -680,7 +689,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (staged) {
       nbar_sync(W::BAR_C, W::CT);
       if (io.ctid < 32) trace_ev(A, j, 7);
-      if (io.ctid == 0) {
+      if (io.ctid == IOT) {
         // Q first: once its bulk read is done the input buffer is free; the residual store is
         // waited for only before the next residual load (after the next volume contraction)
         fence_proxy_async();
@@ -699,12 +708,12 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       // full tiles: this thread refills the buffer (its Q store has been read, or, without a
       // store, nobody reads it any more); the partial last tile is loaded by the producers,
       // who wait for consumer warp 0 to signal the buffer free
-      if (io.ctid == 0 && j + 2 < io.nmine && tile_full(j + 2)) fetch_in(j + 2);
-      if (j + 2 < io.nmine && !tile_full(j + 2) && io.ctid < 32) {
+      if (io.ctid == IOT && j + 2 < io.nmine && tile_full(j + 2)) fetch_in(j + 2);
+      if (j + 2 < io.nmine && !tile_full(j + 2) && (io.ctid >> 5) == IOW) {
         __syncwarp();
         nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
       }
-    } else if (j + W::NIN < io.nmine && io.ctid < 32) {
+    } else if (j + W::NIN < io.nmine && (io.ctid >> 5) == IOW) {
       // only consumer warp 0 signals the Q buffer free (after BAR_C and its lane 0 saw the Q
       // bulk read finish)
       __syncwarp();
@@ -712,7 +721,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
   }
   // make the last bulk stores globally visible before the kernel ends
-  if (io.ctid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (io.ctid == IOT) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 template <int N, int MODE>
