@@ -172,8 +172,22 @@ def run_ours(args):
         s.step(dt, args.steps)
         e1.record(stream)
         barrier()
-    launches = dg.dg_launch_count(s.ctx) - n0
-    ms = e0.elapsed_time(e1)
+        launches = dg.dg_launch_count(s.ctx) - n0
+        ms = e0.elapsed_time(e1)
+        # nvidia-smi samples every 200 ms: a timed region shorter than ~1 s is followed, inside
+        # the sampling window, by untimed repeats of the same steps so the clocks are read under
+        # this workload (same count on every rank: the steps exchange halos)
+        reps = min(2000, int(1000.0 / max(ms, 1e-3)) + 1) if ms < 1000.0 else 0
+        if world > 1:
+            r = torch.tensor([reps], dtype=torch.int64, device=dev)
+            dist.all_reduce(r, op=dist.ReduceOp.MAX)
+            reps = int(r.item())
+        for _ in range(reps):
+            s.step(dt, args.steps)
+        barrier()
+    clk_info = clk.summary()
+    if reps:
+        clk_info["window"] = f"timed region + {reps * args.steps} untimed steps of the same workload"
     dg.dg_check(s.ctx, s.stream)
     ms_max = ms
     if world > 1:
@@ -244,7 +258,7 @@ def run_ours(args):
                          "hbm_bytes_per_elem_stage": bytes_per_elem_stage(cfg.order),
                          "hbm_frac": round(bytes_per_elem_stage(cfg.order) * K_loc / (per_launch_ms * 1e-3) / 1e9
                                            / measured_peaks().get("hbm_gbs", 6545.0), 4)},
-            "clocks": clk.summary(),
+            "clocks": clk_info,
             "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                     "d2h_bytes_per_step": state_bytes, "steps": e2e_steps,
                     "api": "dg_set_state(host pinned) + dg_rk_step(1) + dg_get_state(host pinned)"},
