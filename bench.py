@@ -147,6 +147,9 @@ def run_ours(args):
         uid = [dg.dg_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dg.dg_comm_init(s.ctx, uid[0], world)
+    if args.reserve_sms:
+        # leave SMs free for the NCCL halo kernels so they overlap the interior launch
+        s.set_max_ctas(torch.cuda.get_device_properties(dev).multi_processor_count - args.reserve_sms)
     x = s.nodes()
     Q0 = configs.initial_state(cfg, x)                  # synthetic state at the library's nodes
     s.set_state(Q0)
@@ -196,6 +199,25 @@ def run_ours(args):
         ms_max = float(t.item())
     K_tot = m.K
     dofs = K_tot * s.Np * 5
+    ranks_info = None
+    if world > 1:
+        # per-rank evidence for the scaling run: own stage time, halo size, halo-only time
+        nh = max(1, args.steps)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        h0.record(stream)
+        for _ in range(nh):
+            dg.dg_halo_exchange(s.ctx, s.stream)
+        h1.record(stream)
+        barrier()
+        npeer, nsend, nrecv = dg.dg_halo_info(s.ctx)
+        mine = {"rank": rank, "elements": int(s.K), "ms_steps": round(ms, 4),
+                "ms_per_stage": round(ms / (STAGES * args.steps), 5), "peers": npeer,
+                "halo_send_bytes_per_stage": int(nsend * 5 * s.Nfp * 8),
+                "halo_recv_bytes_per_stage": int(nrecv * 5 * s.Nfp * 8),
+                "halo_only_ms_per_exchange": round(h0.elapsed_time(h1) / nh, 5)}
+        ranks_info = [None] * world
+        dist.all_gather_object(ranks_info, mine)
     value = dofs * STAGES * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---------------- stage-kernel timing on its own stream (roofline numerator)
@@ -264,7 +286,12 @@ def run_ours(args):
                     "api": "dg_set_state(host pinned) + dg_rk_step(1) + dg_get_state(host pinned)"},
             "gpu_launches": int(launches),
             "cpu_baseline": cpu,
+            "build": dg.dg_build_info(),
         }
+        if ranks_info is not None:
+            line["ranks"] = ranks_info
+        if args.reserve_sms:
+            line["config"]["reserve_sms"] = args.reserve_sms
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -307,18 +334,29 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def _cpu_seconds():
+    r = os.times()
+    return r.user + r.system
+
+
 def cpu_baseline(args, cfg, budget_s=12.0):
     nsample = 4096 if cfg.order >= 5 else 16384
     o, stage = _oracle_sample_step(cfg, nsample)
     stage()                                            # warm
     t0 = time.perf_counter()
+    c0 = _cpu_seconds()
     n = 0
     while time.perf_counter() - t0 < budget_s or n == 0:
         stage()
         n += 1
-    dt = (time.perf_counter() - t0) / n
+    wall = time.perf_counter() - t0
+    dt = wall / n
     value = nsample * o.Np * 5 / dt / 1e9
-    return {"value": round(value, 6), "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+    # cores actually used: process CPU time / wall time (numpy's elementwise work is
+    # single-threaded; only the matrix products use the BLAS threads)
+    used = (_cpu_seconds() - c0) / wall
+    return {"value": round(value, 6), "unit": UNIT, "cores": round(used, 2), "kind": "oracle",
+            "blas_threads": cpu_cores(), "host_cpus": os.cpu_count(),
             "sample": f"{n} oracle LSERK4 stages (rhs + update) over {nsample} contiguous elements of {args.config}, "
                       f"{dt:.3f} s/stage"}
 
@@ -333,9 +371,12 @@ def run_reference(args):
     for _ in range(args.warmup):
         stage()
     t0 = time.perf_counter()
+    c0 = _cpu_seconds()
     for _ in range(args.steps):
         stage()
-    dt = (time.perf_counter() - t0) / args.steps
+    wall = time.perf_counter() - t0
+    used = (_cpu_seconds() - c0) / wall
+    dt = wall / args.steps
     value = nsample * o.Np * 5 / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus,
@@ -344,7 +385,8 @@ def run_reference(args):
         "data": "synthetic (seeded)",
         "config": {"workload": f"{args.config} (oracle sample of {nsample} elements, one RK stage per step)",
                    "elements": int(cfg.mesh.K), "order": cfg.order},
-        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "kind": "oracle", "cores": cpu_cores(),
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "kind": "oracle", "cores": round(used, 2),
+                         "blas_threads": cpu_cores(), "host_cpus": os.cpu_count(),
                          "sample": f"{nsample} contiguous elements of {args.config}, 1 LSERK4 stage per step"},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -362,7 +404,24 @@ def main():
     ap.add_argument("--scheme", default="nodal", choices=["nodal", "modal"],
                     help="modal = the paper's modal-quadrature scheme (orders 1-3; SURVEY N3)")
     ap.add_argument("--order", type=int, default=0, help="override the config's polynomial order")
+    ap.add_argument("--reserve-sms", type=int, default=0,
+                    help="stage-kernel grid = SMs - k (leave SMs to the NCCL halo kernels, N > 1)")
     args = ap.parse_args()
+    # run-time experiment switches would change what is timed: refuse them (the build's own
+    # compile-time configuration is recorded in the JSON line as "build")
+    dg_env = sorted(k for k in os.environ if k.startswith("DG_"))
+    if dg_env:
+        raise SystemExit(f"bench.py refuses to run with DG_* experiment variables set: {dg_env}")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: spawn the N ranks ourselves (one process per GPU, NCCL);
+        # rank 0 prints the JSON line
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3

@@ -85,19 +85,31 @@ typedef struct dg_mesh_desc {
                              /* (default), 1 = per node (reading A4)               */
   int check_every;           /* dg_rk_step checks the blow-up flag every n steps (0 = never) */
   int rk_scheme;             /* DG_RK_LSERK4 (default) or DG_RK_HEUN                         */
-  double inflow_alpha;       /* pulse angular frequency of the inflow BC, 565   */
+  double inflow_alpha;       /* pulse angular frequency of the inflow BC: rad per */
+                             /* physical second; <= 0 = the paper's 565 (A24)     */
   int scheme;                /* DG_SCHEME_NODAL (default) or DG_SCHEME_MODAL: the state of   */
                              /* dg_set_state / dg_get_state / dg_rhs stays nodal values at   */
                              /* the dg_get_nodes points; internally the modal scheme steps   */
                              /* orthonormal coefficients (interpolation c = V^-1 u, A23)     */
+  double inflow_time_scale;  /* physical seconds per scaled time unit for the inflow pulse:  */
+                             /* p1 uses cos(alpha * time_scale * t); <= 0 = 2.915e-5 (1 cm / */
+                             /* 343 m/s); 1.0 makes alpha rad per scaled unit    */
+  double inflow_half_amplitude; /* a of p1 = p0 (1 + a - a cos(...)); <= 0 = 0.05 */
 } dg_mesh_desc;
+/* Inflow ghost (Eqs. 5-7) in the units of q_inf: p0 = p(q_inf), rho0 = q_inf[0],
+ * c0 = sqrt(gamma p0 / rho0); rho = rho0 (p/p0)^(1/gamma) (Eq. 6 with C = rho0 p0^(-1/gamma),
+ * = gamma at the paper's p0 = 1, rho0 = 1.4), u = (p - p0)/(rho0 c0) (Eq. 5), v = w = 0.
+ * q_inf must be a valid state (finite, rho > 0, p > 0) when the mesh has pass-through or
+ * inflow faces (else DG_EARG); otherwise it is unused. */
 
 /* Build a context for `rank` (0 <= rank < nparts): validate the mesh, fix or
  * reject orientation (a J <= 0 tet is repaired by swapping its local vertices
- * 2 and 3 only when etoe == NULL, else DG_EMESH), derive/check connectivity,
- * build the reference operators (fp64, orthonormal Jacobi basis), geometric
- * factors, trace pairing and this rank's halo lists.  Host arrays are only read
- * during the call; the caller keeps ownership.  No device work. */
+ * 2 and 3 only when etoe == NULL, else DG_EMESH; the repair moves the tags of
+ * its faces f1 and f3 with the vertex sets the swap exchanges, so bc stays in
+ * the caller's face numbering), derive/check connectivity, build the reference
+ * operators (fp64, orthonormal Jacobi basis), geometric factors, trace pairing
+ * and this rank's halo lists.  Host arrays are only read during the call; the
+ * caller keeps ownership.  No device work. */
 dg_status dg_mesh_create(const dg_mesh_desc* desc, int rank, dg_ctx** out);
 void dg_destroy(dg_ctx* ctx);
 const char* dg_last_error(const dg_ctx* ctx);
@@ -138,6 +150,15 @@ dg_status dg_rhs(dg_ctx* ctx, double t, double* out, void* stream);
  * check_every steps (0 = never) and raises DG_EBLOWUP with the element id. */
 dg_status dg_rk_step(dg_ctx* ctx, double dt, int nsteps, void* stream);
 
+/* Cap the number of CTAs (one per SM) of the persistent stage kernels; 0 = one per SM of the
+ * device (default).  A smaller grid makes every CTA walk more element tiles -- the tests use it to
+ * reach the pipelined steady state on small meshes -- and leaves SMs free for concurrent work
+ * (e.g. the NCCL halo kernels, see dg_rk_step).  Results do not depend on it. */
+dg_status dg_set_max_ctas(dg_ctx* ctx, int max_ctas);
+
+/* Compile-time configuration of this build ("key=value;..."), for benchmark records. */
+const char* dg_build_info(void);
+
 /* Synchronously read the device blow-up flag (DG_EBLOWUP if set). */
 dg_status dg_check(dg_ctx* ctx, void* stream);
 
@@ -172,6 +193,11 @@ dg_status dg_halo_records(const dg_ctx* ctx, int64_t* send_gid, int8_t* send_fac
  * the interior (which & 1) and/or boundary (which & 2) elements; then finish
  * the stage (swap state buffers, advance t after the last stage). */
 dg_status dg_stage_pack(dg_ctx* ctx, void* stream);
+/* Pack + NCCL exchange of the current state's partition-face traces (what every stage of
+ * dg_rk_step does before its boundary launch); the receive buffer is complete when `stream`
+ * reaches its current point.  No-op on one partition.  Needs dg_comm_init.  For timing the
+ * halo alone (bench.py) and for custom stage drivers. */
+dg_status dg_halo_exchange(dg_ctx* ctx, void* stream);
 dg_status dg_stage_compute(dg_ctx* ctx, int s, double dt, int which, void* stream);
 dg_status dg_stage_finish(dg_ctx* ctx, int s, double dt);
 /* same, for one RHS evaluation into `out` (public layout) */

@@ -94,6 +94,31 @@ def ghost_inflow(p_hat, gamma: float = 1.4, p0: float = 1.0, rho0: float = 1.4, 
     return np.stack([rho, rho * u, np.zeros_like(rho), np.zeros_like(rho), E])
 
 
+def inflow_state(t, q_inf, gamma: float, alpha: float = 565.0, time_scale: float = 2.915e-5,
+                 half_amplitude: float = 0.05) -> np.ndarray:
+    """Inflow ghost of Eqs. 5-7 in the units of the ambient state q_inf
+    (reading A24), the form the library evaluates:
+
+      p0 = p(q_inf), rho0 = q_inf[0], c0 = sqrt(gamma p0 / rho0)
+      p  = p0 (1 + a - a cos(alpha tau t)) while alpha tau t < 2 pi, else p0
+      rho = rho0 (p / p0)^(1/gamma)                                           (Eq. 6)
+      u = (p - p0) / (rho0 c0), v = w = 0                                     (Eq. 5)
+      E = p / (gamma - 1) + rho u^2 / 2                                       (Eq. 7)
+
+    tau = physical seconds per scaled time unit (1 cm / 343 m/s), alpha in rad per
+    physical second.  At the paper's constants (q_inf = Eq. 3, a = 0.05, tau = 1) this is
+    ghost_inflow(inflow_pressure(t, alpha)) -- the printed Eq. 7 with C = gamma."""
+    q_inf = np.asarray(q_inf, dtype=np.float64)
+    p0 = float(pressure(q_inf, gamma))
+    rho0 = float(q_inf[0])
+    c0 = np.sqrt(gamma * p0 / rho0)
+    wt = alpha * time_scale * float(t)
+    p = p0 * (1.0 + half_amplitude - half_amplitude * np.cos(wt)) if wt < 2.0 * np.pi else p0
+    rho = rho0 * (p / p0) ** (1.0 / gamma)
+    u = (p - p0) / (rho0 * c0)
+    return np.array([rho, rho * u, 0.0, 0.0, p / (gamma - 1.0) + 0.5 * rho * u * u])
+
+
 def llf_lambda(qm: np.ndarray, qp: np.ndarray, n: np.ndarray, gamma: float) -> np.ndarray:
     """Per-node max(|u-.n| + c-, |u+.n| + c+)."""
     def speed(q):

@@ -57,3 +57,19 @@ def node_coordinates(vxyz: np.ndarray, etov: np.ndarray, r, s, t) -> np.ndarray:
     V = element_vertices(np.asarray(vxyz, dtype=np.float64), np.asarray(etov))
     w = np.stack([-(1 + r + s + t), 1 + r, 1 + s, 1 + t], axis=0) / 2   # (4, Np)
     return np.einsum("vn,kvd->dkn", w, V)
+
+
+def repair_orientation(vxyz: np.ndarray, etov: np.ndarray, bc: np.ndarray):
+    """Negative-volume tets repaired by swapping two vertices; the ABI fixes which
+    (include/dg.h: local vertices 2 and 3, i.e. EToV columns 1 and 2).  The swap exchanges the
+    vertex sets of faces f1 = (v1 v2 v4) and f3 = (v1 v3 v4) (f0 and f2 keep theirs), so the
+    caller's boundary tags, given in the input face numbering, move with them.
+    Returns (etov, bc, flipped)."""
+    V = element_vertices(np.asarray(vxyz, dtype=np.float64), np.asarray(etov))
+    A = np.stack([(V[:, 1] - V[:, 0]) / 2, (V[:, 2] - V[:, 0]) / 2, (V[:, 3] - V[:, 0]) / 2], axis=2)
+    flip = np.linalg.det(A) < 0
+    etov = np.array(etov, dtype=np.int64, copy=True)
+    bc = np.array(bc, copy=True)
+    etov[flip, 1], etov[flip, 2] = etov[flip, 2].copy(), etov[flip, 1].copy()
+    bc[flip, 1], bc[flip, 3] = bc[flip, 3].copy(), bc[flip, 1].copy()
+    return etov, bc, flip

@@ -43,7 +43,7 @@ from scipy.special import roots_jacobi
 
 from . import euler
 from .refelem import DPS, _exponents, _vol_integral
-from .rhs import BC_INFLOW, BC_PASSTHROUGH, BC_WALL, BlowUp, OracleMesh
+from .rhs import BC_INFLOW, BC_PASSTHROUGH, BC_WALL, BlowUp, OracleMesh, ambient_pressure
 
 FACE_VERTS = ((0, 1, 2), (0, 1, 3), (1, 2, 3), (0, 2, 3))
 
@@ -183,7 +183,7 @@ class ModalOracle:
         m, g, gamma = self.m, self.m.geo, self.m.gamma
         K = m.K
         c = np.asarray(c, dtype=np.float64)
-        p_ref = float(euler.pressure(np.asarray(m.q_inf, dtype=np.float64), gamma))
+        p_ref = ambient_pressure(m)
         # volume: u at the quadrature points, contravariant fluxes, weak-form integral
         Uq = c @ self.Pq.T                                   # (5, K, NQ)
         rho, uu, vv, ww, pp = euler.primitives(Uq, gamma)
@@ -212,8 +212,9 @@ class ModalOracle:
                     up[:, sel] = ghost(um[:, sel], n[:, sel])
             sel = tags[:, f] == BC_INFLOW
             if np.any(sel):
-                p1 = np.full(um[0, sel].shape, float(euler.inflow_pressure(t, m.inflow_alpha)))
-                up[:, sel] = euler.ghost_inflow(p1, gamma)
+                qi = euler.inflow_state(t, m.q_inf, gamma, m.inflow_alpha, m.inflow_time_scale,
+                                        m.inflow_half_amplitude)
+                up[:, sel] = qi[:, None]
             lam = euler.llf_lambda(um, up, n, gamma)         # (K, NQF)
             if m.lambda_mode == 0:
                 lam = lam.max(axis=1, keepdims=True)

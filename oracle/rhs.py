@@ -55,6 +55,8 @@ class OracleMesh:
     etof: np.ndarray | None = None
     lambda_mode: int = 0
     inflow_alpha: float = 565.0
+    inflow_time_scale: float = 2.915e-5      # physical s per scaled time unit (reading A24)
+    inflow_half_amplitude: float = 0.05
     _maps: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
@@ -103,6 +105,16 @@ class OracleMesh:
         return self._maps[key]
 
 
+def ambient_pressure(mesh) -> float:
+    """p(q_inf), subtracted from the momentum fluxes (reading A14); 0 when q_inf is not a valid
+    state (it is then unused: no pass-through or inflow face)."""
+    q = np.asarray(mesh.q_inf, dtype=np.float64)
+    if not (np.all(np.isfinite(q)) and q[0] > 0):
+        return 0.0
+    p = float(euler.pressure(q, mesh.gamma))
+    return p if np.isfinite(p) and p > 0 else 0.0
+
+
 def _check_state(mesh: OracleMesh, q: np.ndarray, elems: np.ndarray, t: float):
     rho, u, v, w, p = euler.primitives(q, mesh.gamma)
     bad = ~(np.isfinite(q).all(axis=0) & (rho > 0) & (p > 0))
@@ -121,7 +133,7 @@ def rhs(mesh: OracleMesh, Q: np.ndarray, t: float = 0.0, elems=None) -> np.ndarr
     Qe = Q[:, e]
     _check_state(mesh, Qe, e, t)
 
-    p_ref = float(euler.pressure(np.asarray(mesh.q_inf, dtype=np.float64), gamma))
+    p_ref = ambient_pressure(mesh)
 
     # steps 2-3: volume term
     F, G, H = euler.euler_fluxes(Qe, gamma, p_ref)
@@ -144,9 +156,10 @@ def rhs(mesh: OracleMesh, Q: np.ndarray, t: float = 0.0, elems=None) -> np.ndarr
     if np.any(pt):
         qp[:, pt] = euler.ghost_passthrough(qm[:, pt], mesh.q_inf)
     inf = tag == BC_INFLOW
-    if np.any(inf):                                 # NEXT row N1, scaled units of Eq. 3 only
-        p1 = np.full(qm[0, inf].shape, float(euler.inflow_pressure(t, mesh.inflow_alpha)))
-        qp[:, inf] = euler.ghost_inflow(p1, gamma)
+    if np.any(inf):                                 # NEXT row N1, Eqs. 5-7 (reading A24)
+        qi = euler.inflow_state(t, mesh.q_inf, gamma, mesh.inflow_alpha, mesh.inflow_time_scale,
+                                mesh.inflow_half_amplitude)
+        qp[:, inf] = qi[:, None]
 
     # steps 5-6: LLF flux
     lam = euler.llf_lambda(qm, qp, n, gamma)        # (E, 4, Nfp)

@@ -32,6 +32,7 @@ SYMBOLS = (
     "dg_halo_buffers", "dg_halo_records", "dg_stage_pack", "dg_stage_compute", "dg_stage_finish", "dg_rhs_compute",
     "dg_get_operators", "dg_get_maps", "dg_get_geometry", "dg_launch_count",
     "dg_sensors_set", "dg_sensors_sample", "dg_sensors_record", "dg_sensors_recorded",
+    "dg_set_max_ctas", "dg_build_info", "dg_halo_exchange",
 )
 
 
@@ -60,6 +61,8 @@ class dg_mesh_desc(C.Structure):
         ("rk_scheme", C.c_int),
         ("inflow_alpha", C.c_double),
         ("scheme", C.c_int),
+        ("inflow_time_scale", C.c_double),
+        ("inflow_half_amplitude", C.c_double),
     ]
 
 
@@ -104,6 +107,9 @@ def _load():
         "dg_sensors_sample": (I, [P, P, I, P]),
         "dg_sensors_record": (I, [P, P, I64]),
         "dg_sensors_recorded": (I64, [P]),
+        "dg_set_max_ctas": (I, [P, I]),
+        "dg_build_info": (C.c_char_p, []),
+        "dg_halo_exchange": (I, [P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -145,7 +151,7 @@ def _check(status, ctx=None):
 # ---------------------------------------------------------------- C-named wrappers
 def dg_mesh_create(order, vxyz, etov, bc, *, etoe=None, etof=None, gamma=1.4, q_inf=(1.4, 0, 0, 0, 2.5),
                    part=None, nparts=1, rank=0, lambda_mode=0, check_every=0, rk_scheme=DG_RK_LSERK4,
-                   inflow_alpha=565.0, scheme=DG_SCHEME_NODAL):
+                   inflow_alpha=565.0, scheme=DG_SCHEME_NODAL, inflow_time_scale=0.0, inflow_half_amplitude=0.0):
     """Returns an opaque ctx handle (int).  Host arrays are copied by the library."""
     vxyz = np.ascontiguousarray(vxyz, dtype=np.float64)
     etov = np.ascontiguousarray(etov, dtype=np.int64)
@@ -172,6 +178,8 @@ def dg_mesh_create(order, vxyz, etov, bc, *, etoe=None, etof=None, gamma=1.4, q_
     d.rk_scheme = int(rk_scheme)
     d.inflow_alpha = float(inflow_alpha)
     d.scheme = int(scheme)
+    d.inflow_time_scale = float(inflow_time_scale)
+    d.inflow_half_amplitude = float(inflow_half_amplitude)
     out = C.c_void_p()
     _check(_lib.dg_mesh_create(C.byref(d), int(rank), C.byref(out)))
     return out.value
@@ -235,6 +243,14 @@ def dg_rk_step(ctx, dt: float, nsteps: int, stream: int):
     _check(_lib.dg_rk_step(ctx, float(dt), int(nsteps), stream), ctx)
 
 
+def dg_set_max_ctas(ctx, max_ctas: int):
+    _check(_lib.dg_set_max_ctas(ctx, int(max_ctas)), ctx)
+
+
+def dg_build_info() -> str:
+    return _lib.dg_build_info().decode()
+
+
 def dg_check(ctx, stream: int):
     _check(_lib.dg_check(ctx, stream), ctx)
 
@@ -281,6 +297,10 @@ def dg_halo_records(ctx):
     _check(_lib.dg_halo_records(ctx, _ptr(sg, C.c_int64), _ptr(sf, C.c_int8), _ptr(rg, C.c_int64),
                                 _ptr(rf, C.c_int8)), ctx)
     return sg, sf, rg, rf
+
+
+def dg_halo_exchange(ctx, stream: int):
+    _check(_lib.dg_halo_exchange(ctx, stream), ctx)
 
 
 def dg_stage_pack(ctx, stream: int):
@@ -406,6 +426,10 @@ class Solver:
         if device:
             return out
         return out.cpu().numpy()
+
+    def set_max_ctas(self, n: int):
+        """Cap the stage-kernel grid (0 = one CTA per SM); results do not depend on it."""
+        dg_set_max_ctas(self.ctx, n)
 
     def step(self, dt: float, nsteps: int = 1):
         dg_rk_step(self.ctx, dt, nsteps, self.stream)

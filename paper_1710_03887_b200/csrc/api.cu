@@ -60,59 +60,73 @@ void coeffs(const dg_ctx* c, int s, double& a, double& b, double& cc) {
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
-int g_num_sms = 0;
+// per-device SM count and kernel-attribute state (a process may drive contexts on several GPUs)
+constexpr int MAXDEV = 64;
+int g_num_sms[MAXDEV] = {0};
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < MAXDEV ? dev : 0;
+}
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  const int dev = cur_dev();
+  if (!g_num_sms[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_num_sms[dev] = n > 0 ? n : 148;
   }
-  return g_num_sms;
+  return g_num_sms[dev];
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember it per kernel and device
+template <typename F>
+cudaError_t ensure_smem_attr(F* kern, size_t smem, uint64_t& done_mask) {
+  const int dev = cur_dev();
+  if (done_mask >> dev & 1) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e == cudaSuccess) done_mask |= uint64_t(1) << dev;
+  return e;
+}
+// persistent stage grid: one CTA per SM, capped by the ctx's max_ctas (dg_set_max_ctas)
+int stage_grid(int ntiles, int max_ctas) {
+  int g = std::min(ntiles, num_sms());
+  if (max_ctas > 0) g = std::min(g, max_ctas);
+  return g;
 }
 
 // ---------------------------------------------------------------- kernel dispatch
 template <int N, int MODE>
-cudaError_t launch_ho_n(const dgk::StageArgs& A, cudaStream_t st) {
+cudaError_t launch_ho_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   using H = dgk::HO<N>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgk::stage_ho_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::stage_ho_kernel<N, MODE>, H::SMEM, attr);
+  if (e != cudaSuccess) return e;
   const int ntiles = (A.e_end - A.e_begin + H::EB - 1) / H::EB;
   if (ntiles <= 0) return cudaSuccess;
-  const int grid = std::min(ntiles, num_sms());
-  dgk::stage_ho_kernel<N, MODE><<<grid, H::NT, H::SMEM, st>>>(A);
+  dgk::stage_ho_kernel<N, MODE><<<stage_grid(ntiles, max_ctas), H::NT, H::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 
 template <int N, int MODE>
-cudaError_t launch_ws_n(const dgk::StageArgs& A, cudaStream_t st) {
+cudaError_t launch_ws_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   using W = dgk::WS<N>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgk::stage_ws_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::stage_ws_kernel<N, MODE>, W::SMEM, attr);
+  if (e != cudaSuccess) return e;
   const int ntiles = (A.e_end - A.e_begin + W::EB - 1) / W::EB;
   if (ntiles <= 0) return cudaSuccess;
-  const int grid = std::min(ntiles, num_sms());
-  dgk::stage_ws_kernel<N, MODE><<<grid, W::NT, W::SMEM, st>>>(A);
+  dgk::stage_ws_kernel<N, MODE><<<stage_grid(ntiles, max_ctas), W::NT, W::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_stage(int N, const dgk::StageArgs& A, cudaStream_t st) {
+cudaError_t launch_stage(int N, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   switch (N) {
-    case 1: return launch_ws_n<1, MODE>(A, st);
-    case 2: return launch_ws_n<2, MODE>(A, st);
-    case 3: return launch_ws_n<3, MODE>(A, st);
-    case 4: return launch_ws_n<4, MODE>(A, st);
-    case 5: return launch_ho_n<5, MODE>(A, st);
-    case 6: return launch_ho_n<6, MODE>(A, st);
+    case 1: return launch_ws_n<1, MODE>(A, max_ctas, st);
+    case 2: return launch_ws_n<2, MODE>(A, max_ctas, st);
+    case 3: return launch_ws_n<3, MODE>(A, max_ctas, st);
+    case 4: return launch_ws_n<4, MODE>(A, max_ctas, st);
+    case 5: return launch_ho_n<5, MODE>(A, max_ctas, st);
+    case 6: return launch_ho_n<6, MODE>(A, max_ctas, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -136,27 +150,25 @@ cudaError_t launch_pack(dg_ctx* c, cudaStream_t st) {
 const std::vector<double>& op_host(const dg_ctx* c) { return c->scheme == DG_SCHEME_MODAL ? c->modal_cat : c->opfrag; }
 
 template <int P, int MODE>
-cudaError_t launch_modal_p(const dgk::StageArgs& A, cudaStream_t st) {
+cudaError_t launch_modal_p(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   using W = dgk::MW<P>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgk::modal_warp_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::modal_warp_kernel<P, MODE>, W::SMEM, attr);
+  if (e != cudaSuccess) return e;
   const int nel = A.e_end - A.e_begin;
   if (nel <= 0) return cudaSuccess;
-  const int grid = std::min((nel + W::WPC * W::EPW - 1) / (W::WPC * W::EPW), 8 * num_sms());
+  int grid = std::min((nel + W::WPC * W::EPW - 1) / (W::WPC * W::EPW), 8 * num_sms());
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);
   dgk::modal_warp_kernel<P, MODE><<<grid, W::NT, W::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_modal(int P, const dgk::StageArgs& A, cudaStream_t st) {
+cudaError_t launch_modal(int P, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   switch (P) {
-    case 1: return launch_modal_p<1, MODE>(A, st);
-    case 2: return launch_modal_p<2, MODE>(A, st);
-    case 3: return launch_modal_p<3, MODE>(A, st);
+    case 1: return launch_modal_p<1, MODE>(A, max_ctas, st);
+    case 2: return launch_modal_p<2, MODE>(A, max_ctas, st);
+    case 3: return launch_modal_p<3, MODE>(A, max_ctas, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -202,12 +214,15 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   A.gamma = c->gamma;
   A.t = t;
   for (int i = 0; i < 5; ++i) A.qinf[i] = c->q_inf[i];
-  A.inflow_alpha = c->inflow_alpha;
+  // inflow ghost constants (reading A24): ambient state = q_inf (validated when used)
+  A.in_p0 = c->qinf_valid ? c->pref : 1.0;
+  A.in_rho0 = c->qinf_valid ? c->q_inf[0] : 1.4;
+  A.in_c0 = std::sqrt(c->gamma * A.in_p0 / A.in_rho0);
+  A.in_amp = c->inflow_half_amplitude * A.in_p0;
+  A.in_omega = c->inflow_alpha * c->inflow_time_scale;
   A.lambda_mode = c->lambda_mode;
-  if (const char* dbg = std::getenv("DG_DEBUG_TIMING")) A.debug = std::atoi(dbg);
   A.trace = reinterpret_cast<unsigned long long*>(c->dscratch);
-  const double* qi = c->q_inf;
-  A.pref = (c->gamma - 1.0) * (qi[4] - 0.5 * (qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]) / qi[0]);
+  A.pref = c->pref;
   return A;
 }
 
@@ -250,8 +265,8 @@ dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st)
   A.dt = dt;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, st)
-                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, st));
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, c->max_ctas, st)
+                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, c->max_ctas, st));
     ++c->launches;
   }
   return DG_OK;
@@ -461,6 +476,53 @@ dg_status dg_get_time(const dg_ctx* c, double* t) {
   return DG_OK;
 }
 
+dg_status dg_set_max_ctas(dg_ctx* c, int max_ctas) {
+  if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
+  if (max_ctas < 0) return set_err(c, DG_EARG, "max_ctas must be >= 0");
+  if (c->max_ctas != max_ctas)
+    for (void*& g : c->graph_exec)   // captured steps carry the old grid
+      if (g) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
+        g = nullptr;
+      }
+  c->max_ctas = max_ctas;
+  return DG_OK;
+}
+
+#define DG_STR2(x) #x
+#define DG_STR(x) DG_STR2(x)
+const char* dg_build_info(void) {
+  return "arch=sm_100a;DG_TRACE=" DG_STR(DG_TRACE) ";DG_DEBUG_SKIP=" DG_STR(DG_DEBUG_SKIP)
+#ifdef DG_WS_PW
+         ";DG_WS_PW=" DG_STR(DG_WS_PW)
+#endif
+#ifdef DG_WS_CW
+         ";DG_WS_CW=" DG_STR(DG_WS_CW)
+#endif
+#ifdef DG_WS_EB
+         ";DG_WS_EB=" DG_STR(DG_WS_EB)
+#endif
+#ifdef DG_KUNROLL
+         ";DG_KUNROLL=" DG_STR(DG_KUNROLL)
+#endif
+#ifdef DG_NEWTON2
+         ";DG_NEWTON2=1"
+#endif
+#ifdef DG_SKIP_VOL
+         ";DG_SKIP_VOL=" DG_STR(DG_SKIP_VOL)
+#endif
+#ifdef DG_WS_IOW
+         ";DG_WS_IOW=" DG_STR(DG_WS_IOW)
+#endif
+#ifdef DG_HO_KC
+         ";DG_HO_KC=" DG_STR(DG_HO_KC)
+#endif
+#ifdef DG_HO_SLOTS
+         ";DG_HO_SLOTS=" DG_STR(DG_HO_SLOTS)
+#endif
+         ";DG_SDF=" DG_STR(DG_SDF) ";DG_HO_SDF=" DG_STR(DG_HO_SDF);
+}
+
 dg_status dg_check(dg_ctx* c, void* stream) {
   dg_status s0 = need_bound(c);
   if (s0) return s0;
@@ -486,8 +548,8 @@ dg_status dg_rhs_compute(dg_ctx* c, double t, double* out, int which, void* stre
   A.out = out;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, st)
-                                             : launch_stage<dgk::MODE_RHS>(c->N, A, st));
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, c->max_ctas, st)
+                                             : launch_stage<dgk::MODE_RHS>(c->N, A, c->max_ctas, st));
     ++c->launches;
   }
   return DG_OK;
@@ -506,6 +568,18 @@ dg_status dg_rhs(dg_ctx* c, double t, double* out, void* stream) {
     return dg_rhs_compute(c, t, out, 2, stream);
   }
   return dg_rhs_compute(c, t, out, 3, stream);
+}
+
+dg_status dg_halo_exchange(dg_ctx* c, void* stream) {
+  dg_status s0 = need_bound(c);
+  if (s0) return s0;
+  if (!c->state_set) return set_err(c, DG_ESTATE, "state not set");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (c->nparts == 1 || c->peers.empty()) return DG_OK;
+  dg_status e = halo_exchange(c, st);
+  if (e) return e;
+  CUDA_TRY(c, cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(c->ev_recvd), 0));
+  return DG_OK;
 }
 
 dg_status dg_stage_pack(dg_ctx* c, void* stream) {

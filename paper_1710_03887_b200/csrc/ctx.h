@@ -20,7 +20,10 @@ struct dg_ctx {
   double gamma = 1.4;
   double q_inf[5] = {1.4, 0, 0, 0, 2.5};
   int lambda_mode = 0, check_every = 0, rk_scheme = DG_RK_LSERK4;
-  double inflow_alpha = 565.0;
+  double inflow_alpha = 565.0, inflow_time_scale = 2.915e-5, inflow_half_amplitude = 0.05;
+  double pref = 0.0;              // ambient pressure p(q_inf) subtracted from the fluxes (A14), 0 if unused
+  bool qinf_valid = false;
+  int max_ctas = 0;               // stage-kernel grid cap (0 = one CTA per SM)
   int scheme = DG_SCHEME_NODAL;
   dgb::RefElem ref;
   dgb::ModalTables modal;           // scheme == DG_SCHEME_MODAL

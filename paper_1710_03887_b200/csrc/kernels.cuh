@@ -58,9 +58,10 @@ struct StageArgs {
   double gamma, a, b, dt, t;
   double pref;            // ambient pressure subtracted from the momentum fluxes (exact, A14)
   double qinf[5];
-  double inflow_alpha;
+  // inflow ghost (Eqs. 5-7; reading A24): ambient p0, rho0, c0 from q_inf
+  // and gamma, pulse half amplitude in pressure units, angular frequency per scaled time unit
+  double in_p0, in_rho0, in_c0, in_amp, in_omega;
   int lambda_mode;
-  int debug;              // timing experiments only: 1 = skip DMMA, 2 = skip flux math
   unsigned long long* trace;   // DG_TRACE builds: per-phase clock64 stamps of CTA 0
 };
 
@@ -94,6 +95,11 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 #ifndef DG_TRACE
 #define DG_TRACE 0
 #endif
+// Timing experiments only, compile time (tools/debug_sweep.sh builds with -DDG_DEBUG_SKIP=n):
+// 1 = skip the DMMA contraction, 2 = skip the flux arithmetic.  Product builds: 0.
+#ifndef DG_DEBUG_SKIP
+#define DG_DEBUG_SKIP 0
+#endif
 __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   if (DG_TRACE && blockIdx.x == 0 && j < 64 && A.trace) {
     __syncwarp();
@@ -120,16 +126,21 @@ __device__ __forceinline__ void flag_blowup(int* flag, int64_t gid) {
   if (atomicCAS(flag, 0, 1) == 0) flag[1] = (int)gid;
 }
 
-// Eq. 5-7 inflow ghost (paper's scaled units), NEXT row N1
-__device__ __forceinline__ void inflow_state(double t, double alpha, double gamma, double (&q)[5]) {
-  double p = (t < 2.0 * M_PI / alpha) ? 1.0 + (0.05 - 0.05 * cos(alpha * t)) : 1.0;
-  double rho = gamma * pow(p, 1.0 / gamma);
-  double u = (p - 1.0) / (1.4 * 1.0);
+// Eqs. 5-7 inflow ghost (NEXT row N1; reading A24):
+//   p = p0 + (a - a cos(omega t)) for omega t < 2 pi, else p0      (scaled p0 = 1, a = 0.05)
+//   rho = rho0 (p / p0)^(1/gamma)                                   (Eq. 6, C = gamma at rho0 = 1.4, p0 = 1)
+//   u = (p - p0) / (rho0 c0),  v = w = 0                            (Eq. 5)
+//   E = p / (gamma - 1) + rho u^2 / 2                               (Eq. 7)
+__device__ __forceinline__ void inflow_state(const StageArgs& A, double (&q)[5]) {
+  const double wt = A.in_omega * A.t;
+  const double p = (wt < 2.0 * M_PI) ? A.in_p0 + (A.in_amp - A.in_amp * cos(wt)) : A.in_p0;
+  const double rho = A.in_rho0 * pow(p / A.in_p0, 1.0 / A.gamma);
+  const double u = (p - A.in_p0) / (A.in_rho0 * A.in_c0);
   q[0] = rho;
   q[1] = rho * u;
   q[2] = 0.0;
   q[3] = 0.0;
-  q[4] = p / (gamma - 1.0) + 0.5 * rho * u * u;
+  q[4] = p / (A.gamma - 1.0) + 0.5 * rho * u * u;
 }
 
 enum { MODE_UPDATE = 0, MODE_RHS = 1 };
@@ -203,7 +214,7 @@ __device__ __forceinline__ void ghost_trace(const StageArgs& A, int tag, const d
 #pragma unroll
     for (int c = 0; c < 5; ++c) qp[c] = A.qinf[c];
   } else {
-    inflow_state(A.t, A.inflow_alpha, A.gamma, qp);
+    inflow_state(A, qp);
   }
 }
 
@@ -260,7 +271,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
     const int e = face >> 2, f = face & 3;
 #pragma unroll
     for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
-    if (!(A.debug & 2) && lane_ok && face < flim && e < ne) {
+    if (!(DG_DEBUG_SKIP & 2) && lane_ok && face < flim && e < ne) {
       const int code = c_s[e * 4 + f];
       if (code < CODE_BC) {
         gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
@@ -288,7 +299,7 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
                                            bool lane_ok, const double* q_s, const double* g_s, const uint8_t* sFm,
                                            const double (&qp)[NPASS][5], double* sXf) {
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
-  if (A.debug & 2) return;
+  if (DG_DEBUG_SKIP & 2) return;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
   double rip[NPASS], unp[NPASS], pp[NPASS], lam[NPASS], unmv[NPASS], pmv[NPASS];
 #pragma unroll
@@ -566,7 +577,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     };
     auto kloop = [&](auto xblk) {
       constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
-      if (A.debug & 1) return;
+      if (DG_DEBUG_SKIP & 1) return;
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
       constexpr int KU = kunroll<N>();
 #pragma unroll KU
@@ -687,6 +698,9 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
     if (io.ctid < 32) trace_ev(A, j, 6);
     if (staged) {
+      // every thread that wrote the staged tiles orders its generic-proxy stores before the
+      // async-proxy (TMA) reads of the bulk stores issued after the barrier
+      fence_proxy_async();
       nbar_sync(W::BAR_C, W::CT);
       if (io.ctid < 32) trace_ev(A, j, 7);
       if (io.ctid == IOT) {
@@ -834,7 +848,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 #endif
 #pragma unroll
       for (int r0 = 0; r0 < VR; r0 += 2) {
-        if (A.debug & 2) break;
+        if (DG_DEBUG_SKIP & 2) break;
 #pragma unroll
         for (int rr = r0; rr < r0 + 2 && rr < VR; ++rr) {
           if constexpr (SKIPV) {
@@ -1144,7 +1158,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       const int e = face >> 2, f = face & 3;
 #pragma unroll
       for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
-      if (!(A.debug & 2) && lane_ok && face < EB * 4 && e < ne) {
+      if (!(DG_DEBUG_SKIP & 2) && lane_ok && face < EB * 4 && e < ne) {
         const int code = c_s[e * 4 + f];
         if (code < CODE_BC) {
           gather_trace<NP, NFP>(A, code, n_s[e * 4 + f], f, i, sTbl, sTblf, qp[u]);
@@ -1164,7 +1178,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     nbar_sync(1, CT);
     if (warp == 0) trace_ev(A, j, 3);
     // ---- volume fluxes -> X[:, 0:3Np)
-    if (!(A.debug & 2)) {
+    if (!(DG_DEBUG_SKIP & 2)) {
       constexpr int VR = (EB * NP + CT - 1) / CT;
 #pragma unroll
       for (int rr = 0; rr < VR; ++rr) {
@@ -1194,7 +1208,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
     }
     if (warp == 0) trace_ev(A, j, 4);
     // ---- face terms -> X[:, KVP:KVP+4Nfp)
-    if (!(A.debug & 2)) {
+    if (!(DG_DEBUG_SKIP & 2)) {
       double rip[H::FPASS], unp[H::FPASS], pp[H::FPASS], lam[H::FPASS], unmv[H::FPASS], pmv[H::FPASS];
 #pragma unroll
       for (int u = 0; u < H::FPASS; ++u) {
@@ -1290,7 +1304,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       wfull += clock64() - tw0;
 #endif
       const double* ob = ring + size_t(s) * (H::BCH / 8) + (it.kind == 0 ? it.p * 64 : H::NPG * 64);
-      if (!(A.debug & 1)) {
+      if (!(DG_DEBUG_SKIP & 1)) {
         // compile-time shape per item and chunk length: unpredicated DMMAs, loads hoisted
         auto run = [&](auto kcn) {
           constexpr int KCN = decltype(kcn)::value;
@@ -1378,6 +1392,7 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       }
     }
     if (warp == 0) trace_ev(A, j, 9);
+    if (staged) fence_proxy_async();   // each writer: generic stores before the TMA store reads
     nbar_sync(1, CT);   // staging complete; q_s of this tile no longer read
     if (tid == 0 && staged) {
       fence_proxy_async();

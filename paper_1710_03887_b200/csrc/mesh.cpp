@@ -60,6 +60,25 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   c->check_every = d->check_every;
   c->rk_scheme = d->rk_scheme;
   c->inflow_alpha = d->inflow_alpha > 0 ? d->inflow_alpha : 565.0;
+  c->inflow_time_scale = d->inflow_time_scale > 0 ? d->inflow_time_scale : 2.915e-5;
+  c->inflow_half_amplitude = d->inflow_half_amplitude > 0 ? d->inflow_half_amplitude : 0.05;
+  if (!std::isfinite(c->inflow_alpha) || !std::isfinite(c->inflow_time_scale) || !std::isfinite(c->inflow_half_amplitude))
+    return fail(c, DG_EARG, "inflow parameters must be finite");
+  {
+    // q_inf: the pass-through ghost (Eq. 3) and the inflow ambient state; its pressure is the
+    // background subtracted from the fluxes (A14).  Decided over the whole mesh, so every rank
+    // of a partition uses the same pref (bitwise partition invariance).
+    const double* q = d->q_inf;
+    bool fin = true;
+    for (int i = 0; i < 5; ++i) fin &= std::isfinite(q[i]);
+    const double p = fin && q[0] > 0 ? (d->gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]) : 0.0;
+    c->qinf_valid = fin && q[0] > 0 && p > 0 && std::isfinite(p);
+    c->pref = c->qinf_valid ? p : 0.0;
+    bool used = false;
+    for (int64_t i = 0; i < 4 * d->k && !used; ++i) used = d->bc[i] == DG_BC_PASSTHROUGH || d->bc[i] == DG_BC_INFLOW;
+    if (used && !c->qinf_valid)
+      return fail(c, DG_EARG, "q_inf must be a valid state (finite, rho > 0, p > 0): the mesh has pass-through or inflow faces");
+  }
   std::string msg;
   if (!build_reference(c->N, c->ref, &msg)) return fail(c, DG_EARG, "reference element: " + msg);
   if (d->scheme != DG_SCHEME_NODAL && d->scheme != DG_SCHEME_MODAL) return fail(c, DG_EARG, "unknown scheme");
@@ -79,6 +98,7 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
 
   // ---- vertices per element, orientation
   std::vector<int64_t> etov(d->etov, d->etov + 4 * K);
+  std::vector<int8_t> bcv(d->bc, d->bc + 4 * K);   // tags in the (repaired) face numbering
   for (int64_t i = 0; i < 4 * K; ++i)
     if (etov[i] < 0 || etov[i] >= nv) return fail(c, DG_EMESH, "EToV references an unknown vertex (element " + std::to_string(i / 4) + ")");
   auto vert = [&](int64_t v) { return V3{d->vxyz[3 * v], d->vxyz[3 * v + 1], d->vxyz[3 * v + 2]}; };
@@ -98,6 +118,9 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
       if (J == 0.0 || !std::isfinite(J)) return fail(c, DG_EMESH, "degenerate element " + std::to_string(k) + " (J = 0)");
       if (d->etoe) return fail(c, DG_EMESH, "element " + std::to_string(k) + " has J <= 0 and connectivity was given");
       std::swap(etov[4 * k + 1], etov[4 * k + 2]);   // S:89 repair
+      // the swap exchanges the vertex sets of faces f1 (v1 v2 v4) and f3 (v1 v3 v4): their
+      // tags, given in the caller's face numbering, move with them
+      std::swap(bcv[4 * k + 1], bcv[4 * k + 3]);
     }
   }
 
@@ -148,7 +171,7 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   for (int64_t k = 0; k < K; ++k)
     for (int f = 0; f < 4; ++f) {
       bool bnd = etoe[4 * k + f] == k && etof[4 * k + f] == f;
-      int tag = d->bc[4 * k + f];
+      int tag = bcv[4 * k + f];
       if (bnd && (tag < DG_BC_WALL || tag > DG_BC_INFLOW))
         return fail(c, DG_EMESH, "boundary face without a valid tag (element " + std::to_string(k) + ", face " + std::to_string(f) + ")");
       if (!bnd && tag != DG_BC_INTERIOR)
@@ -178,7 +201,7 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   // boundary range merely wait for the halo
   c->K_int = int64_t(inter.size()) / 32 * 32;
   for (int64_t k : mine)
-    for (int f = 0; f < 4; ++f) c->has_inflow |= d->bc[4 * k + f] == DG_BC_INFLOW;
+    for (int f = 0; f < 4; ++f) c->has_inflow |= bcv[4 * k + f] == DG_BC_INFLOW;
   c->gid = inter;
   c->gid.insert(c->gid.end(), bound.begin(), bound.end());
   std::vector<int64_t> g2l(K, -1), g2pub(K, -1);
@@ -264,7 +287,7 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
       const int64_t k2 = etoe[4 * k + f];
       const int f2 = etof[4 * k + f];
       if (k2 == k && f2 == f) {
-        c->code[l * 4 + f] = uint8_t(64 + d->bc[4 * k + f]);
+        c->code[l * 4 + f] = uint8_t(64 + bcv[4 * k + f]);
         continue;
       }
       V3 P[3], Q[3], cP, cQ;

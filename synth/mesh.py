@@ -165,3 +165,62 @@ def x_slab_partition(mesh: TetMesh, nparts: int) -> np.ndarray:
     for p in range(nparts):
         part[order[bounds[p]:bounds[p + 1]]] = p
     return part
+
+
+# local vertex opposite each face (FACES[f] = the other three) and the face opposite each vertex
+OPPOSITE = np.array([3, 2, 0, 1])
+FACE_OF_OPPOSITE = np.argsort(OPPOSITE)            # vertex v -> the face not containing it
+_PERMS4 = np.array(list(permutations(range(4))))
+_EVEN4 = np.array([p for p in _PERMS4 if round(np.linalg.det(np.eye(4)[list(p)])) > 0])
+
+
+def relabel_vertices(mesh: TetMesh, seed: int, even_only: bool = True) -> TetMesh:
+    """Random local vertex order per tet (an unstructured-mesh input, like GMSH output):
+    new etov[k][i] = old etov[k][perm_k[i]].  Faces are renumbered consistently (EToE/EToF/bc
+    permuted by the induced face map).  even_only keeps every J > 0 (even permutations preserve
+    orientation); odd permutations flip J < 0, which the library repairs only when it derives
+    the connectivity itself (etoe = NULL)."""
+    rng = np.random.default_rng(seed)
+    K = mesh.K
+    pool = _EVEN4 if even_only else _PERMS4
+    perm = pool[rng.integers(0, len(pool), K)]                    # (K, 4)
+    inv = np.argsort(perm, axis=1)
+    etov = np.take_along_axis(mesh.etov, perm, axis=1)
+    # old face f excludes old vertex OPPOSITE[f], whose new local index is inv[OPPOSITE[f]]
+    nf = FACE_OF_OPPOSITE[np.take_along_axis(inv, np.broadcast_to(OPPOSITE, (K, 4)), axis=1)]   # (K, 4)
+    etoe = np.empty_like(mesh.etoe)
+    etof = np.empty_like(mesh.etof)
+    bc = np.empty_like(mesh.bc)
+    rows = np.arange(K)[:, None]
+    k2 = mesh.etoe
+    f2new = nf[k2, mesh.etof]
+    etoe[rows, nf] = k2
+    etof[rows, nf] = f2new
+    bc[rows, nf] = mesh.bc
+    out = TetMesh(vxyz=mesh.vxyz, etov=etov, etoe=etoe, etof=etof, bc=bc, period=mesh.period, info=dict(mesh.info))
+    out.info["relabelled"] = {"seed": seed, "even_only": even_only}
+    return out
+
+
+def face_orientation_codes(mesh: TetMesh, part=None):
+    """Set of (f, f2, sigma) over the paired faces (optionally only the faces whose two elements
+    lie on different ranks of `part`), sigma = the tuple m -> m' such that vertex m of face f
+    of k coincides with vertex m' of face f2 of its neighbour (positions relative to the face
+    centroids, so periodic translations pair too).  For coverage counts in the tests."""
+    codes = set()
+    v = mesh.vxyz[mesh.etov]                                        # (K, 4, 3)
+    for k in range(mesh.K):
+        for f in range(4):
+            k2, f2 = int(mesh.etoe[k, f]), int(mesh.etof[k, f])
+            if k2 == k and f2 == f:
+                continue
+            if part is not None and part[k] == part[k2]:
+                continue
+            P = v[k, FACES[f]]
+            Qv = v[k2, FACES[f2]]
+            P = P - P.mean(axis=0)
+            Qv = Qv - Qv.mean(axis=0)
+            d = np.linalg.norm(P[:, None, :] - Qv[None, :, :], axis=2)
+            sig = tuple(int(j) for j in d.argmin(axis=1))
+            codes.add((f, f2, sig))
+    return codes

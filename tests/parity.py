@@ -33,10 +33,25 @@ def e_state(gpu, ora, S):
     return (np.abs(gpu - ora).reshape(5, -1).max(axis=1) / S).max()
 
 
-def oracle_mesh(cfg, lambda_mode=0):
+def oracle_mesh(cfg, lambda_mode=0, **kw):
     m = cfg.mesh
     return OracleMesh(order=cfg.order, vxyz=m.vxyz, etov=m.etov, bc=m.bc, etoe=m.etoe, etof=m.etof,
-                      gamma=cfg.gamma, q_inf=cfg.q_inf, lambda_mode=lambda_mode)
+                      gamma=cfg.gamma, q_inf=cfg.q_inf, lambda_mode=lambda_mode, **kw)
+
+
+# Stage-kernel grid caps the multi-step tests run under (dg_set_max_ctas): 0 = one CTA per SM
+# (the bench launch configuration; on the oracle-sized meshes <= 1 tile per CTA), 2 and 7 = every
+# CTA walks many tiles, so the pipelined steady state -- TMA prefetch of the next tiles, input
+# refills two tiles ahead, residual tiles arriving a tile early, the partial last tile landing on
+# a CTA's j >= 2 -- meets the oracle too.
+GRID_CAPS = (0, 2, 7)
+
+
+def tiles_per_cta(K, order, cap):
+    eb = 32 if order <= 2 else 16 if order <= 4 else 8
+    nt = -(-K // eb)
+    grid = min(nt, 148) if cap == 0 else min(nt, 148, cap)
+    return -(-nt // grid)
 
 
 def oracle_dt(o: OracleMesh, Q, cfl):

@@ -60,9 +60,9 @@ def _state(o, cfg):
 @pytest.mark.parametrize("periodic", [False, True])
 def test_modal_rhs_parity(p, lambda_mode, periodic):
     cfg = _case(p, p, periodic)
-    o = modal.ModalOracle(parity.oracle_mesh(cfg, lambda_mode))
+    o = modal.ModalOracle(parity.oracle_mesh(cfg, lambda_mode, inflow_time_scale=1.0))
     Q = _state(o, cfg)
-    s = _solver(cfg, lambda_mode=lambda_mode)
+    s = _solver(cfg, lambda_mode=lambda_mode, inflow_time_scale=1.0)   # alpha per scaled unit
     s.set_state(Q)
     t = 0.002
     want = o.to_nodal(o.rhs(o.to_modal(Q), t))
@@ -72,12 +72,14 @@ def test_modal_rhs_parity(p, lambda_mode, periodic):
     s.close()
 
 
-def test_modal_rk_parity_100_steps():
+@pytest.mark.parametrize("cap", [0, 1])
+def test_modal_rk_parity_100_steps(cap):
     cfg = _case(2, 7, periodic=True)
     o = modal.ModalOracle(parity.oracle_mesh(cfg))
     Q = _state(o, cfg)
     dt = 0.5 * parity.oracle_dt(o.m, Q, 0.5)
     s = _solver(cfg)
+    s.set_max_ctas(cap)
     s.set_state(Q)
     s.step(dt, 100)
     c, _, _ = timestep.integrate(lambda cc, tt: o.rhs(cc, tt), o.to_modal(Q), 0.0, dt, 100)
@@ -101,4 +103,24 @@ def test_modal_sensors_and_dt():
         want = sensors.sample(2, Q, k, r, ss, t, cfg.gamma)
         assert np.abs(got[i] - want).max() < 1e-12
     assert abs(s.stable_dt(0.5) - parity.oracle_dt(o.m, Q, 0.5)) < 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("rk", ["lserk4", "heun"])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_modal_inflow_through_the_stepper(rk, p):
+    """The inflow ghost at every stage time (reading A20) in the modal scheme: 30 steps with the
+    pulse lasting 20 dt (rise, fall and switch-off inside the run)."""
+    cfg = _case(p, 5)
+    o0 = parity.oracle_mesh(cfg)
+    Q = _state(modal.ModalOracle(o0), cfg)
+    dt = 0.5 * parity.oracle_dt(o0, Q, 0.4)
+    kw = dict(inflow_alpha=2 * np.pi / (20 * dt), inflow_time_scale=1.0)
+    o = modal.ModalOracle(parity.oracle_mesh(cfg, **kw))
+    s = _solver(cfg, rk_scheme=dg.DG_RK_HEUN if rk == "heun" else dg.DG_RK_LSERK4, **kw)
+    s.set_state(Q)
+    s.step(dt, 30)
+    c, _, _ = timestep.integrate(lambda cc, tt: o.rhs(cc, tt), o.to_modal(Q), 0.0, dt, 30, scheme=rk)
+    err = parity.e_state(s.get_state(), o.to_nodal(c), parity.scales(cfg))
+    assert err <= parity.STATE_TOL, err
     s.close()

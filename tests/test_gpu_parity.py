@@ -4,11 +4,17 @@ Same seeded inputs on both sides (synth/ recipes at the ORACLE's node
 coordinates); tolerances from BASELINE.json (tests/parity.py):
   one RHS <= 1e-11 (scaled), 100 LSERK4 steps <= 1e-9.
 Sizes: oracle-sized versions of C1-C5 that span several tiles and a ragged
-tail; full-size C2-C5 in the bench launch configuration on sampled elements;
-edge cases (one element, ragged tails, every boundary kind, lambda modes,
-Heun, inflow), blow-up detection, state round trip, and partition invariance
-(emulated ranks on one GPU, exchange by device copies).
+tail, stepped under several stage-grid caps (parity.GRID_CAPS) so every CTA
+walks many tiles (the pipelined steady state the bench times); full-size C2-C5
+in the bench launch configuration on sampled elements through all five LSERK4
+stages; full-size C2 for 100 steps against a committed oracle run
+(tests/golden/make_c2_100.py); edge cases (one element, ragged tails, every
+boundary kind, lambda modes, Heun, inflow through the stepper), relabelled and
+inverted unstructured-style meshes (all 48 reachable face-orientation codes),
+blow-up detection, state round trip, and partition invariance (emulated ranks
+on one GPU, exchange by device copies, one-launch and interior/boundary split).
 """
+import os
 import numpy as np
 import pytest
 
@@ -17,11 +23,15 @@ pytestmark = pytest.mark.gpu
 
 import paper_1710_03887_b200 as dg  # noqa: E402
 from oracle import timestep  # noqa: E402
+from oracle.rhs import OracleMesh  # noqa: E402
 from oracle.rhs import rhs as oracle_rhs  # noqa: E402
 from synth import configs  # noqa: E402
 from synth import mesh as smesh  # noqa: E402
 
+import meshes  # noqa: E402
 import parity  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 SMALL = [("C1", 1.0), ("C2", 0.25), ("C3", 0.15), ("C4", 0.1), ("C5", 0.1)]
 
@@ -56,26 +66,34 @@ def test_rhs_parity_small(name, scale, lambda_mode):
 
 @pytest.mark.parametrize("name,scale", SMALL)
 def test_rk_parity_100_steps(name, scale):
+    """100 LSERK4 steps <= 1e-9 (BASELINE.json north_star; eq:ode P:415-419), once per grid cap:
+    the default grid (<= 1 tile per CTA on these sizes) and capped grids where every CTA walks
+    >= 4 tiles through the cross-tile pipeline, with the residual path (a_s != 0) live."""
     cfg = configs.make(name, scale=scale)
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
     dt = parity.oracle_dt(o, Q, cfg.cfl)
-    s = solver(cfg)
-    s.set_state(Q)
-    s.step(dt, 100)
-    g = s.get_state()
     Qo, _, t = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 100)
-    err = parity.e_state(g, Qo, parity.scales(cfg))
-    assert err <= parity.STATE_TOL, err
-    assert abs(s.time - t) < 1e-12 * max(1.0, t)
+    assert parity.tiles_per_cta(cfg.mesh.K, cfg.order, 2) >= 4
+    for cap in parity.GRID_CAPS:
+        s = solver(cfg)
+        s.set_max_ctas(cap)
+        s.set_state(Q)
+        s.step(dt, 100)
+        err = parity.e_state(s.get_state(), Qo, parity.scales(cfg))
+        assert err <= parity.STATE_TOL, (cap, err)
+        assert abs(s.time - t) < 1e-12 * max(1.0, t)
+        s.close()
 
 
-def test_heun_parity():
+@pytest.mark.parametrize("cap", [0, 3])
+def test_heun_parity(cap):
     cfg = configs.make("C3", scale=0.15)
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
     dt = parity.oracle_dt(o, Q, 0.3)
     s = solver(cfg, rk_scheme=dg.DG_RK_HEUN)
+    s.set_max_ctas(cap)
     s.set_state(Q)
     s.step(dt, 20)
     Qo, _, _ = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 20, scheme="heun")
@@ -96,11 +114,11 @@ def test_every_order_and_boundary_kind(N):
     m.bc[bnd & (cen[:, 0:1] < 0.2)] = smesh.BC_INFLOW
     cfg = configs.Config("box", N, m, rho0=1.4, p0=1.0, gamma=1.4,
                          pulses=[(0.05, 0.2, (0.5, 0.35, 0.35))], steps=1)
-    o = parity.oracle_mesh(cfg)
+    o = parity.oracle_mesh(cfg, inflow_time_scale=1.0)
     Q = configs.initial_state(cfg, o.x)
     Q[1] += 0.05 * Q[0] * np.sin(3 * o.x[1])          # some flow so every ghost matters
     Q[4] += 0.5 * (Q[1] ** 2) / Q[0]
-    s = solver(cfg)
+    s = solver(cfg, inflow_time_scale=1.0)             # alpha = 565 rad per scaled unit
     s.set_state(Q)
     t = 0.002                                           # inside the inflow pulse
     err = parity.e_rhs(s.rhs(t), oracle_rhs(o, Q, t), parity.scales(cfg))
@@ -158,8 +176,11 @@ def test_blowup_flag_names_the_element():
 
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_full_size_sampled(name):
-    """Full BASELINE.json size, bench launch configuration; oracle on sampled elements:
-    one RHS, and stage 0 of the LSERK update (res = dt f, Q += b_0 res)."""
+    """Full BASELINE.json size, bench launch configuration; oracle on sampled elements: one RHS,
+    then all five LSERK4 stages through dg_stage_compute.  Each stage's input state is read back
+    on the sample and its neighbours, the oracle forms f on the sample from it, carries its own
+    residual res_s = a_s res_(s-1) + dt f and predicts Q_(s+1) = Q_s + b_s res_s; stages 1-4 run
+    the a_s != 0 residual path in the pipelined steady state (~20-70 tiles per CTA)."""
     cfg = configs.make(name)
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
@@ -175,16 +196,149 @@ def test_full_size_sampled(name):
     hot = np.argsort(amp)[-40:]
     sample = np.unique(np.concatenate([rng.choice(K, 160, replace=False), hot, wall[:24], pt[:24],
                                        np.arange(K - 9, K), np.arange(0, 5)]))
-    g = s.rhs(0.0, device=True)[:, torch.as_tensor(sample, device=s.device)].cpu().numpy()
+    patch = np.unique(np.concatenate([sample, cfg.mesh.etoe[sample].ravel()]))
+    dsample = torch.as_tensor(sample, device=s.device)
+    dpatch = torch.as_tensor(patch, device=s.device)
+    g = s.rhs(0.0, device=True)[:, dsample].cpu().numpy()
     r = oracle_rhs(o, Q, 0.0, elems=sample)
     S = parity.scales(cfg)
     assert parity.e_rhs(g, r, S) <= parity.RHS_TOL
-    dt = 1e-3
-    dg.dg_stage_compute(s.ctx, 0, dt, 3, s.stream)
-    dg.dg_stage_finish(s.ctx, 0, dt)
-    Q1 = s.get_state(device=True)[:, torch.as_tensor(sample, device=s.device)].cpu().numpy()
-    want = Q[:, sample] + timestep.LSERK4_B[0] * (dt * r)
-    assert parity.e_state(Q1, want, S) <= 1e-14
+    dt = parity.oracle_dt(o, Q, cfg.cfl)
+    Qh = np.zeros_like(Q)
+    Qh[:, patch] = Q[:, patch]
+    res = np.zeros((5, len(sample), o.Np))
+    pos = np.searchsorted(patch, sample)
+    for st in range(5):
+        f = oracle_rhs(o, Qh, timestep.LSERK4_C[st] * dt, elems=sample)
+        res = timestep.LSERK4_A[st] * res + dt * f
+        want = Qh[:, sample] + timestep.LSERK4_B[st] * res
+        dg.dg_stage_compute(s.ctx, st, dt, 3, s.stream)
+        dg.dg_stage_finish(s.ctx, st, dt)
+        Qp = s.get_state(device=True)[:, dpatch].cpu().numpy()
+        err = parity.e_state(Qp[:, pos], want, S)
+        assert err <= 1e-13, (st, err)
+        Qh[:, patch] = Qp
+    assert abs(s.time - dt) < 1e-15
+
+
+def test_c2_full_size_100_steps_golden():
+    """Full-size C2 (24,576 tets, ~10 tiles per CTA at the default grid) for 100 LSERK4 steps
+    through dg_rk_step (CUDA-graph replay), against the committed oracle run
+    tests/golden/c2_lserk4_100.npz: the final state of 512 elements (<= 1e-9) and full-field
+    properties of the whole GPU state (mass, energy, max deviation from ambient); then again
+    with the grid capped at 7 CTAs (~220 tiles per CTA)."""
+    gold = np.load(os.path.join(GOLDEN, "c2_lserk4_100.npz"))
+    cfg = configs.make("C2")
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    S = parity.scales(cfg)
+    wts = o.ref.M.sum(axis=1)
+    qinf = np.asarray(cfg.q_inf)[:, None, None]
+    for cap in (0, 7):
+        s = solver(cfg)
+        s.set_max_ctas(cap)
+        s.set_state(Q)
+        s.step(float(gold["dt"]), int(gold["nsteps"]))
+        G = s.get_state()
+        assert abs(s.time - float(gold["t_end"])) < 1e-13
+        err = parity.e_state(G[:, gold["elems"]], gold["Q_elems"], S)
+        assert err <= parity.STATE_TOL, (cap, err)
+        mass = np.sum(o.geo.J[:, None] * wts[None, :] * G[0])
+        energy = np.sum(o.geo.J[:, None] * wts[None, :] * G[4])
+        assert abs(mass - float(gold["mass"])) <= 1e-12 * abs(float(gold["mass"]))
+        assert abs(energy - float(gold["energy"])) <= 1e-12 * abs(float(gold["energy"]))
+        dev = np.abs(G - qinf).reshape(5, -1).max(axis=1)
+        assert np.all(np.abs(dev - gold["dev_max"]) <= parity.STATE_TOL * S)
+        s.close()
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 0.25), ("C4", 0.1), ("C5", 0.1)])
+def test_relabelled_meshes(name, scale):
+    """Unstructured-style local vertex orders (all 48 reachable face-orientation codes,
+    tests/meshes.py): one RHS <= 1e-11, 10 LSERK4 steps <= 1e-9 with every CTA walking tiles."""
+    cfg = meshes.relabelled(name, scale)
+    o = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o.x)
+    Q[1] += 0.02 * Q[0] * np.sin(3 * o.x[2] + 0.5)       # flow, so every trace pairing matters
+    Q[4] += 0.5 * Q[1] ** 2 / Q[0]
+    S = parity.scales(cfg)
+    s = solver(cfg)
+    s.set_state(Q)
+    assert parity.e_rhs(s.rhs(0.0), oracle_rhs(o, Q), S) <= parity.RHS_TOL
+    dt = parity.oracle_dt(o, Q, cfg.cfl)
+    Qo, _, _ = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 10)
+    s.set_max_ctas(3)
+    s.step(dt, 10)
+    assert parity.e_state(s.get_state(), Qo, S) <= parity.STATE_TOL
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 0.25), ("C4", 0.1)])
+def test_inverted_mesh_repair(name, scale):
+    """About half the tets inverted, mixed wall / pass-through tags, connectivity left to the
+    library (etoe = NULL): repaired by the S:89 vertex swap with the f1/f3 tags moved along
+    (include/dg.h); the oracle runs on its own repair of the same input."""
+    from oracle import geom as ogeom
+    from oracle.conn import connect_by_hashing
+    cfg = meshes.inverted(name, scale)
+    m = cfg.mesh
+    etov, bc, _ = ogeom.repair_orientation(m.vxyz, m.etov, m.bc)
+    etoe, etof = connect_by_hashing(etov)
+    o = OracleMesh(order=cfg.order, vxyz=m.vxyz, etov=etov, bc=bc, etoe=etoe, etof=etof,
+                   gamma=cfg.gamma, q_inf=cfg.q_inf)
+    Q = configs.initial_state(cfg, o.x)
+    Q[2] += 0.03 * Q[0] * np.cos(2 * o.x[0] + 0.3)
+    Q[4] += 0.5 * Q[2] ** 2 / Q[0]
+    s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, gamma=cfg.gamma, q_inf=cfg.q_inf)   # etoe = NULL
+    assert np.abs(s.nodes() - o.x).max() < 1e-13 * max(1.0, np.abs(o.x).max())
+    s.set_state(Q)
+    S = parity.scales(cfg)
+    assert parity.e_rhs(s.rhs(0.0), oracle_rhs(o, Q), S) <= parity.RHS_TOL
+    dt = parity.oracle_dt(o, Q, cfg.cfl)
+    Qo, _, _ = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 10)
+    s.set_max_ctas(2)
+    s.step(dt, 10)
+    assert parity.e_state(s.get_state(), Qo, S) <= parity.STATE_TOL
+
+
+def inflow_box(N, seed=1):
+    """Distorted box: inflow faces at x = 0 (the paper's mouthpiece), pass-through at
+    x = 1, walls elsewhere."""
+    m = smesh.kuhn_box((4, 2, 2), (0, 0, 0), (1, 0.5, 0.5), bc_tag=smesh.BC_WALL)
+    rng = np.random.default_rng(seed)
+    lo, hi = m.vxyz.min(0), m.vxyz.max(0)
+    inner = np.all((m.vxyz > lo + 1e-9) & (m.vxyz < hi - 1e-9), axis=1)
+    m.vxyz[inner] += rng.uniform(-0.02, 0.02, (int(inner.sum()), 3))
+    cen = m.vxyz[m.etov[:, smesh.FACES]].mean(axis=2)
+    bnd = m.bc != 0
+    m.bc[bnd & (cen[:, :, 0] > 1 - 1e-9)] = smesh.BC_PASSTHROUGH
+    m.bc[bnd & (cen[:, :, 0] < 1e-9)] = smesh.BC_INFLOW
+    return configs.Config("inflow-box", N, m, rho0=1.4, p0=1.0, gamma=1.4, pulses=[], steps=1)
+
+
+@pytest.mark.parametrize("rk", ["lserk4", "heun"])
+@pytest.mark.parametrize("N", [2, 4])
+def test_inflow_through_the_stepper(rk, N):
+    """The time-dependent inflow ghost (Eqs. 5-7; reading A24) evaluated at each
+    stage time t + c_s dt inside dg_rk_step (reading A20): 40 steps with the pulse duration
+    2 pi / (alpha tau) set to 25 dt, so the run covers the rising and falling pulse and the
+    switch-off at t = 2 pi / (alpha tau)."""
+    cfg = inflow_box(N)
+    tau = 1.0
+    o0 = parity.oracle_mesh(cfg)
+    Q = configs.initial_state(cfg, o0.x)
+    dt = parity.oracle_dt(o0, Q, 0.4)
+    alpha = 2 * np.pi / (25 * dt * tau)
+    kw = dict(inflow_alpha=alpha, inflow_time_scale=tau)
+    o = parity.oracle_mesh(cfg, **kw)
+    scheme = dg.DG_RK_HEUN if rk == "heun" else dg.DG_RK_LSERK4
+    s = solver(cfg, rk_scheme=scheme, **kw)
+    s.set_max_ctas(1)
+    s.set_state(Q)
+    s.step(dt, 40)
+    Qo, _, _ = timestep.integrate(lambda q, tt: oracle_rhs(o, q, tt), Q, 0.0, dt, 40, scheme=rk)
+    S = parity.scales(cfg)
+    assert np.abs(Qo - Q).max() > 1e-3                 # the pulse entered the domain
+    assert parity.e_state(s.get_state(), Qo, S) <= parity.STATE_TOL
 
 
 def ws_view(sv, ptr, nbytes):
@@ -193,10 +347,13 @@ def ws_view(sv, ptr, nbytes):
     return sv.ws[off:off + nbytes]
 
 
-@pytest.mark.parametrize("nparts", [2, 3])
-def test_partition_invariance_emulated(nparts):
-    """P ranks emulated as P contexts on one GPU, halo records exchanged by device
-    copies between the stage-level calls: final state bitwise equal to P = 1."""
+@pytest.mark.parametrize("nparts,split,cap", [(2, False, 0), (3, False, 0), (2, True, 0), (3, True, 2)])
+def test_partition_invariance_emulated(nparts, split, cap):
+    """P ranks emulated as P contexts on one GPU, halo records exchanged by device copies
+    between the stage-level calls: final state bitwise equal to P = 1.  split: the
+    production order of dg_rk_step -- pack, interior launch (which = 1) BEFORE the halo
+    arrives, then the boundary launch (which = 2, the range starting at K_int) -- and the
+    same for dg_rhs_compute; cap: every CTA walks several tiles of each range."""
     cfg = configs.make("C4", scale=0.12)
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
@@ -208,13 +365,12 @@ def test_partition_invariance_emulated(nparts):
     part = smesh.x_slab_partition(cfg.mesh, nparts)
     ranks = [solver(cfg, part=part, nparts=nparts, rank=r) for r in range(nparts)]
     for r, sv in enumerate(ranks):
+        sv.set_max_ctas(cap)
         sv.set_state(Q[:, part == r])
     rec = 5 * ranks[0].Nfp
-    for _ in range(10):
-        for st in range(5):
-            for sv in ranks:
-                dg.dg_stage_pack(sv.ctx, sv.stream)
-            for r, sv in enumerate(ranks):
+
+    def exchange():
+        for r, sv in enumerate(ranks):
                 npeer, _, _ = dg.dg_halo_info(sv.ctx)
                 _, rbuf = dg.dg_halo_buffers(sv.ctx)
                 for p in range(npeer):
@@ -229,8 +385,41 @@ def test_partition_invariance_emulated(nparts):
                         dst = ws_view(sv, rbuf + info["recv_off"] * rec * 8, n)
                         src = ws_view(other, sbuf + mine["send_off"] * rec * 8, n)
                         dst.copy_(src)
+
+    # one RHS first (dg_rhs_compute, split or not) against the single-partition RHS
+    ref.set_state(Q)
+    f_ref = ref.rhs(0.0)
+    for sv in ranks:
+        dg.dg_stage_pack(sv.ctx, sv.stream)
+    outs = [torch.zeros((5, sv.K, sv.Np), dtype=torch.float64, device=sv.device) for sv in ranks]
+    if split:
+        for sv, o_ in zip(ranks, outs):
+            dg.dg_rhs_compute(sv.ctx, 0.0, o_.data_ptr(), 1, sv.stream)
+        exchange()
+        for sv, o_ in zip(ranks, outs):
+            dg.dg_rhs_compute(sv.ctx, 0.0, o_.data_ptr(), 2, sv.stream)
+    else:
+        exchange()
+        for sv, o_ in zip(ranks, outs):
+            dg.dg_rhs_compute(sv.ctx, 0.0, o_.data_ptr(), 3, sv.stream)
+    f_got = np.empty_like(f_ref)
+    for r, o_ in enumerate(outs):
+        f_got[:, part == r] = o_.cpu().numpy()
+    assert np.array_equal(f_got, f_ref)
+    for _ in range(10):
+        for st in range(5):
             for sv in ranks:
-                dg.dg_stage_compute(sv.ctx, st, dt, 3, sv.stream)
+                dg.dg_stage_pack(sv.ctx, sv.stream)
+            if split:
+                for sv in ranks:        # interior elements never read the halo
+                    dg.dg_stage_compute(sv.ctx, st, dt, 1, sv.stream)
+                exchange()
+                for sv in ranks:
+                    dg.dg_stage_compute(sv.ctx, st, dt, 2, sv.stream)
+            else:
+                exchange()
+                for sv in ranks:
+                    dg.dg_stage_compute(sv.ctx, st, dt, 3, sv.stream)
             for sv in ranks:
                 dg.dg_stage_finish(sv.ctx, st, dt)
     got = np.empty_like(want)
@@ -239,8 +428,8 @@ def test_partition_invariance_emulated(nparts):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("rk", [dg.DG_RK_LSERK4, dg.DG_RK_HEUN])
-def test_graph_replay_is_bitwise_eager(rk, monkeypatch):
+@pytest.mark.parametrize("rk,cap", [(dg.DG_RK_LSERK4, 0), (dg.DG_RK_HEUN, 0), (dg.DG_RK_LSERK4, 3)])
+def test_graph_replay_is_bitwise_eager(rk, cap, monkeypatch):
     """dg_rk_step replays captured steps as CUDA graphs on one partition; the result must be
     bit-identical to eager launches, across a dt change (graph re-capture) and both integrators."""
     cfg = configs.make("C2", scale=0.25)
@@ -251,6 +440,7 @@ def test_graph_replay_is_bitwise_eager(rk, monkeypatch):
         else:
             monkeypatch.delenv("DG_NO_GRAPHS", raising=False)
         s = solver(cfg, rk_scheme=rk)
+        s.set_max_ctas(cap)
         s.set_state(configs.initial_state(cfg, s.nodes()))
         dt = s.stable_dt(0.4)
         s.step(dt, 7)

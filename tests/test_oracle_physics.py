@@ -114,6 +114,39 @@ def test_inflow_ghost_and_pulse():
     assert float(euler.inflow_pressure(0.0, alpha)) == pytest.approx(1.0, abs=1e-15)
 
 
+def test_inflow_state_generalises_the_printed_eq7():
+    """Reading A24: at the paper's constants (Eq. 3 ambient, a = 0.05, time in the units alpha
+    is given in) the q_inf-relative inflow state is exactly the printed Eq. 7 (P:206-216:
+    rho = gamma p^(1/gamma), u = (p - p0)/(rho0 c)) applied to p1 of P:173-181."""
+    alpha = 565.0
+    for t in (0.0, 0.3 / alpha, math.pi / alpha, 5.9 / alpha, 2 * math.pi / alpha + 1e-9):
+        want = euler.ghost_inflow(euler.inflow_pressure(t, alpha), G)
+        got = euler.inflow_state(t, REST, G, alpha=alpha, time_scale=1.0)
+        assert np.allclose(got, want, rtol=1e-14, atol=1e-15)
+    # another ambient state: the ghost is the same pulse in those units (p0 scales, c0 follows)
+    q2 = np.array([1.225, 0.0, 0.0, 0.0, 101325.0 / 0.4])
+    g2 = euler.inflow_state(math.pi / alpha, q2, G, alpha=alpha, time_scale=1.0)
+    p2 = euler.pressure(g2, G)
+    assert p2 == pytest.approx(1.1 * 101325.0, rel=1e-14)                 # peak p0 (1 + 2a)
+    c0 = math.sqrt(G * 101325.0 / 1.225)
+    assert g2[1] / g2[0] == pytest.approx(0.1 * 101325.0 / (1.225 * c0), rel=1e-14)   # Eq. 5
+    assert g2[0] == pytest.approx(1.225 * 1.1 ** (1 / G), rel=1e-14)                  # Eq. 6
+
+
+def test_inflow_pulse_duration_in_scaled_time():
+    """alpha = 565 rad per physical second, time_scale = 1 cm / 343 m/s
+    = 2.915e-5 s per scaled unit, so the pulse lasts 2 pi / 565 s = 11.12 ms = 381.5 scaled units."""
+    tau = 2.915e-5
+    dur = 2 * math.pi / (565.0 * tau)
+    assert 0.01 / 343.0 == pytest.approx(tau, rel=2e-4)
+    assert 2 * math.pi / 565.0 == pytest.approx(11.12e-3, rel=1e-3)
+    assert dur == pytest.approx(381.5, abs=0.1)
+    peak = euler.inflow_state(dur / 2, REST, G)                # default alpha, tau, a
+    assert euler.pressure(peak, G) == pytest.approx(1.1, rel=1e-12)
+    after = euler.inflow_state(dur * 1.0001, REST, G)
+    assert np.allclose(after, REST, rtol=0, atol=1e-15)
+
+
 def test_paper_constants():
     # Eq. 3 (P:141-152): p0 = 1, rho0 = 1.4 give c0 = 1 and E0 = 2.5
     assert euler.pressure(REST, G) == pytest.approx(1.0)
