@@ -286,7 +286,7 @@ def run_ours(args):
                     "api": "dg_set_state(host pinned) + dg_rk_step(1) + dg_get_state(host pinned)"},
             "gpu_launches": int(launches),
             "cpu_baseline": cpu,
-            "build": dg.dg_build_info(),
+            "build": build_info(dg),
         }
         if ranks_info is not None:
             line["ranks"] = ranks_info
@@ -295,6 +295,13 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def build_info(dg):
+    try:
+        return dg.dg_build_info()
+    except AttributeError:          # an older library build without the call
+        return None
 
 
 # ------------------------------------------------------------------ oracle (CPU)

@@ -214,7 +214,7 @@ class ModalOracle:
             if np.any(sel):
                 qi = euler.inflow_state(t, m.q_inf, gamma, m.inflow_alpha, m.inflow_time_scale,
                                         m.inflow_half_amplitude)
-                up[:, sel] = qi[:, None]
+                up[:, sel] = qi[:, None, None]
             lam = euler.llf_lambda(um, up, n, gamma)         # (K, NQF)
             if m.lambda_mode == 0:
                 lam = lam.max(axis=1, keepdims=True)

@@ -259,8 +259,10 @@ class RefElem:
 
 
 @functools.lru_cache(maxsize=None)
-def reference_element(N: int) -> RefElem:
-    """All nodal operators at order N, exact to fp64 rounding (see module doc)."""
+def reference_element(N: int, dtype=np.float64) -> RefElem:
+    """All nodal operators at order N, exact to fp64 rounding (see module doc).  dtype =
+    np.longdouble rounds the same 50-digit results to x87 extended precision instead (the
+    fp64 noise-floor measurement, oracle/precision.py)."""
     if N < 1:
         raise ValueError("order N must be >= 1")
     with mp.workdps(DPS):
@@ -303,8 +305,12 @@ def reference_element(N: int) -> RefElem:
             Lcols.append(_dot(V, _dot(Ginv, GfCF)))
         LIFT = np.concatenate(Lcols, axis=1)
 
-        def f64(A):
-            return np.array([[float(v) for v in row] for row in A], dtype=np.float64)
+        if dtype == np.float64:
+            def f64(A):
+                return np.array([[float(v) for v in row] for row in A], dtype=np.float64)
+        else:
+            def f64(A):
+                return np.array([[np.longdouble(mp.nstr(v, 30)) for v in row] for row in A], dtype=np.longdouble)
 
         r = np.array([float(2 * l[1] - 1) for l in lam])
         s = np.array([float(2 * l[2] - 1) for l in lam])

@@ -127,7 +127,9 @@ def rhs(mesh: OracleMesh, Q: np.ndarray, t: float = 0.0, elems=None) -> np.ndarr
     """f(Q, t) for the elements ``elems`` (default: all), shape (5, E, Np)."""
     ref, g, gamma = mesh.ref, mesh.geo, mesh.gamma
     K, Np, Nfp = mesh.K, mesh.Np, mesh.Nfp
-    Q = np.asarray(Q, dtype=np.float64)
+    Q = np.asarray(Q)
+    if Q.dtype != np.longdouble:       # longdouble only for the noise floor (oracle/precision.py)
+        Q = Q.astype(np.float64, copy=False)
     assert Q.shape == (5, K, Np)
     e = np.arange(K) if elems is None else np.asarray(elems, dtype=np.int64)
     Qe = Q[:, e]
@@ -159,7 +161,7 @@ def rhs(mesh: OracleMesh, Q: np.ndarray, t: float = 0.0, elems=None) -> np.ndarr
     if np.any(inf):                                 # NEXT row N1, Eqs. 5-7 (reading A24)
         qi = euler.inflow_state(t, mesh.q_inf, gamma, mesh.inflow_alpha, mesh.inflow_time_scale,
                                 mesh.inflow_half_amplitude)
-        qp[:, inf] = qi[:, None]
+        qp[:, inf] = qi[:, None, None]
 
     # steps 5-6: LLF flux
     lam = euler.llf_lambda(qm, qp, n, gamma)        # (E, 4, Nfp)

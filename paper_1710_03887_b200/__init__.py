@@ -112,6 +112,8 @@ def _load():
         "dg_halo_exchange": (I, [P, P]),
     }
     for name, (res, args) in sig.items():
+        if not hasattr(lib, name):   # an older build: the call fails (AttributeError) when used
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

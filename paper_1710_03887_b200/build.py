@@ -52,11 +52,13 @@ def defines() -> dict:
     return {k: os.environ[k] for k in ("DG_WS_PW", "DG_WS_CW", "DG_WS_EB", "DG_HO_KC", "DG_HO_SLOTS", "DG_SDF", "DG_TRACE", "DG_KUNROLL", "DG_NEWTON2", "DG_HO_SDF", "DG_WS_IOW", "DG_SKIP_VOL") if k in os.environ}
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose_ptxas: bool = False, out: str = LIB, extra_defines=None) -> str:
+    """Build the library to `out` (default: the in-tree lib/libdg_b200.so the binding loads);
+    extra_defines (dict) add compile-time experiment knobs (tools/build_variants.py)."""
+    if not force and out == LIB and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    bdir = os.path.join(HERE, "build")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    bdir = os.path.join(HERE, "build" if out == LIB else "build_" + os.path.basename(os.path.dirname(out)))
     os.makedirs(bdir, exist_ok=True)
     nd = nccl_dir()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
@@ -68,11 +70,12 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     o = os.path.join(bdir, "api.cu.o")
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
     extra += [f"-D{k}={v}" for k, v in defines().items()]
+    extra += [f"-D{k}={v}" for k, v in (extra_defines or {}).items()]
     _run([NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                           "-c", os.path.join(CSRC, "api.cu"), "-o", o] + inc + extra)
     objs.append(o)
     ncl = os.path.join(nd, "lib")
-    _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
+    _run([NVCC] + ARCH + ["-shared", "-o", out] + objs +
          ["-L", ncl, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + ncl])
     return LIB
 

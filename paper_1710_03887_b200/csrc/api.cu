@@ -221,6 +221,7 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   A.in_amp = c->inflow_half_amplitude * A.in_p0;
   A.in_omega = c->inflow_alpha * c->inflow_time_scale;
   A.lambda_mode = c->lambda_mode;
+  A.skip = DG_DEBUG_SKIP;   // compile-time (0 in product builds)
   A.trace = reinterpret_cast<unsigned long long*>(c->dscratch);
   A.pref = c->pref;
   return A;

@@ -33,6 +33,28 @@ def e_state(gpu, ora, S):
     return (np.abs(gpu - ora).reshape(5, -1).max(axis=1) / S).max()
 
 
+def e_pert(gpu, ora, q0):
+    """The stricter perturbation form of SURVEY §8(c) A14: max_q |dQ_q|_inf / |Q_q - q0_q|_inf
+    (fields identically at q0, e.g. the momentum of a pulse at rest at t = 0, are skipped)."""
+    q0 = np.asarray(q0, dtype=np.float64).reshape(5, *([1] * (np.ndim(ora) - 1)))
+    d = np.abs(gpu - ora).reshape(5, -1).max(axis=1)
+    m = np.abs(ora - q0).reshape(5, -1).max(axis=1)
+    ok = m > 0
+    return float((d[ok] / m[ok]).max())
+
+
+def record(test, **vals):
+    """Append measured parity numbers to $PARITY_LOG (JSON lines) when it is set (GPU evidence
+    runs: tools/r02_gpu_tests.sh); a no-op otherwise."""
+    import json
+    import os
+    path = os.environ.get("PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": test, **{k: (float(v) if hasattr(v, "__float__") else v)
+                                                 for k, v in vals.items()}}) + "\n")
+
+
 def oracle_mesh(cfg, lambda_mode=0, **kw):
     m = cfg.mesh
     return OracleMesh(order=cfg.order, vxyz=m.vxyz, etov=m.etov, bc=m.bc, etoe=m.etoe, etof=m.etof,

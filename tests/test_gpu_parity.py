@@ -60,6 +60,7 @@ def test_rhs_parity_small(name, scale, lambda_mode):
     g = s.rhs(0.0)
     r = oracle_rhs(o, Q)
     err = parity.e_rhs(g, r, parity.scales(cfg))
+    parity.record(f"rhs[{name}@{scale},lambda{lambda_mode}]", e_rhs=err)
     assert err <= parity.RHS_TOL, err
     assert dg.dg_launch_count(s.ctx) >= 2
 
@@ -80,7 +81,10 @@ def test_rk_parity_100_steps(name, scale):
         s.set_max_ctas(cap)
         s.set_state(Q)
         s.step(dt, 100)
-        err = parity.e_state(s.get_state(), Qo, parity.scales(cfg))
+        G = s.get_state()
+        err = parity.e_state(G, Qo, parity.scales(cfg))
+        parity.record(f"rk100[{name}@{scale}]", cap=cap, e_state=err, e_pert=parity.e_pert(G, Qo, cfg.q_inf),
+                      tiles_per_cta=parity.tiles_per_cta(cfg.mesh.K, cfg.order, cap))
         assert err <= parity.STATE_TOL, (cap, err)
         assert abs(s.time - t) < 1e-12 * max(1.0, t)
         s.close()
@@ -202,7 +206,9 @@ def test_full_size_sampled(name):
     g = s.rhs(0.0, device=True)[:, dsample].cpu().numpy()
     r = oracle_rhs(o, Q, 0.0, elems=sample)
     S = parity.scales(cfg)
-    assert parity.e_rhs(g, r, S) <= parity.RHS_TOL
+    e0 = parity.e_rhs(g, r, S)
+    parity.record(f"full_rhs[{name}]", e_rhs=e0, sample=len(sample))
+    assert e0 <= parity.RHS_TOL
     dt = parity.oracle_dt(o, Q, cfg.cfl)
     Qh = np.zeros_like(Q)
     Qh[:, patch] = Q[:, patch]
@@ -216,6 +222,7 @@ def test_full_size_sampled(name):
         dg.dg_stage_finish(s.ctx, st, dt)
         Qp = s.get_state(device=True)[:, dpatch].cpu().numpy()
         err = parity.e_state(Qp[:, pos], want, S)
+        parity.record(f"full_stage[{name}]", stage=st, e_state=err)
         assert err <= 1e-13, (st, err)
         Qh[:, patch] = Qp
     assert abs(s.time - dt) < 1e-15
@@ -242,6 +249,8 @@ def test_c2_full_size_100_steps_golden():
         G = s.get_state()
         assert abs(s.time - float(gold["t_end"])) < 1e-13
         err = parity.e_state(G[:, gold["elems"]], gold["Q_elems"], S)
+        parity.record("c2_golden_100", cap=cap, e_state=err,
+                      e_pert=parity.e_pert(G[:, gold["elems"]], gold["Q_elems"], cfg.q_inf))
         assert err <= parity.STATE_TOL, (cap, err)
         mass = np.sum(o.geo.J[:, None] * wts[None, :] * G[0])
         energy = np.sum(o.geo.J[:, None] * wts[None, :] * G[4])

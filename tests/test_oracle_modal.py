@@ -76,7 +76,7 @@ def _jiggled(n, seed):
     return dict(vxyz=v, etov=m.etov, bc=m.bc, etoe=m.etoe, etof=m.etof, gamma=G)
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 def test_free_stream_and_conservation(p):
     o = modal.ModalOracle(OracleMesh(order=p, **_jiggled(3, p)))
     q = np.array([1.2, 0.3, -0.2, 0.1, 2.7])
@@ -94,7 +94,7 @@ def test_free_stream_and_conservation(p):
     assert np.all(np.abs(tot) <= 1e-12 * scale), (tot, scale)
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 def test_entropy_wave_convergence(p):
     """rho = rho0 (1 + eps sin 2pi(x - u t)), u and p constant: exact Euler solution."""
     vel = np.array([0.3, 0.2, 0.1])
@@ -119,3 +119,19 @@ def test_entropy_wave_convergence(p):
     rate = math.log(errs[0] / errs[1]) / math.log(2)
     # N + 1/2 is the a-priori bound; coarse meshes run above N + 1 (observed p=1: 3.2)
     assert p + 0.4 <= rate <= p + 2.5, (errs, rate)
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_inflow_faces_after_the_pulse_preserve_rest(p):
+    """Inflow ghost (Eqs. 5-7) once the pulse is over is the ambient state: rest is preserved;
+    during the pulse only elements touching an inflow face feel it (one RHS)."""
+    m = smesh.kuhn_box((3, 2, 2), (0, 0, 0), (1, 1, 1), bc_tag=smesh.BC_WALL)
+    cen = m.vxyz[m.etov[:, smesh.FACES]].mean(axis=2)
+    m.bc[(m.bc != 0) & (cen[:, :, 0] < 1e-9)] = smesh.BC_INFLOW
+    o = modal.ModalOracle(OracleMesh(order=p, vxyz=m.vxyz, etov=m.etov, bc=m.bc, etoe=m.etoe, etof=m.etof,
+                                     gamma=G, inflow_time_scale=1.0))
+    U = np.broadcast_to(np.array([1.4, 0, 0, 0, 2.5])[:, None, None], (5, o.m.K, o.Np)).copy()
+    assert np.abs(o.rhs(o.to_modal(U), 2 * np.pi / 565.0 + 1e-6)).max() < 1e-12
+    f = o.rhs(o.to_modal(U), np.pi / 565.0)
+    touched = (m.bc == smesh.BC_INFLOW).any(axis=1)
+    assert np.abs(f[:, touched]).max() > 1e-3 and np.abs(f[:, ~touched]).max() < 1e-12

@@ -66,6 +66,18 @@ def test_free_stream_preservation(N):
         o = om(m, N, q_inf=REST, lambda_mode=mode)
         f = rhs(o, uniform(o, REST))
         assert (np.abs(f).max(axis=(1, 2)) * o.geo.h.min() / S).max() < 1e-12
+    # inflow faces (Eqs. 5-7) outside the pulse (t >= 2 pi/(alpha tau): p1 = p0) ghost the
+    # ambient state: the rest state is preserved; inside the pulse it is not, and only the
+    # elements that touch an inflow face feel it at t (one RHS, no propagation yet)
+    m = jiggle(smesh.kuhn_box((3, 2, 2), (0, 0, 0), (1, 1, 1), bc_tag=smesh.BC_WALL), 0.05, 3)
+    cen = m.vxyz[m.etov[:, smesh.FACES]].mean(axis=2)
+    m.bc[(m.bc != 0) & (cen[:, :, 0] < 1e-9)] = smesh.BC_INFLOW
+    o = om(m, N, q_inf=REST, inflow_time_scale=1.0)
+    f = rhs(o, uniform(o, REST), t=2 * np.pi / 565.0 + 1e-6)
+    assert (np.abs(f).max(axis=(1, 2)) * o.geo.h.min() / S).max() < 1e-12
+    f = rhs(o, uniform(o, REST), t=np.pi / 565.0)
+    touched = (m.bc == smesh.BC_INFLOW).any(axis=1)
+    assert np.abs(f[:, touched]).max() > 1e-3 and np.abs(f[:, ~touched]).max() < 1e-12
 
 
 def _pulse_state(o, seed, vel=0.05, amp=0.05):
@@ -217,14 +229,14 @@ def _run(o, Q, T, cfl=0.5):
     return Qn
 
 
-@pytest.mark.parametrize("N", [1, 2, 3])
+@pytest.mark.parametrize("N", [1, 2, 3, 4])
 def test_h_convergence_density_wave(N):
     """Exact Euler solution rho = rho0 (1 + eps sin 2pi(x - u t)), velocity and p constant
     (an entropy wave; textbook), on a periodic slab of cubic hexes; L2 rate -> N+1."""
     vel = np.array([0.3, 0.2, 0.1])
     eps, T = 0.1, 0.1
     errs = []
-    ns = {1: (4, 8, 16), 2: (8, 16), 3: (6, 12)}[N]
+    ns = {1: (4, 8, 16), 2: (8, 16), 3: (6, 12), 4: (4, 8, 12)}[N]
     for n in ns:
         m = smesh.kuhn_box((n, 3, 3), (0, 0, 0), (1, 3.0 / n, 3.0 / n), periodic=(True, True, True))
         o = om(m, N)
@@ -237,11 +249,12 @@ def test_h_convergence_density_wave(N):
 
         QT = _run(o, state(0.0), T)
         errs.append(_l2(o, QT[0] - state(T)[0]) / math.sqrt(9.0 / n ** 2))
-    rates = np.log(np.array(errs[:-1]) / np.array(errs[1:])) / np.log(2)
+    rates = np.log(np.array(errs[:-1]) / np.array(errs[1:])) / np.log(np.array(ns[1:]) / np.array(ns[:-1]))
     # Observed: N=1 -> 2.0, N=2 -> 2.6 (3.36 one level finer), N=3 -> 3.45-3.58.  The
     # sharp a-priori bound for upwind-type DG on general meshes is h^(N+1/2)
     # (Johnson-Pitkaranta / Peterson), optimal h^(N+1) is the usual observation; a
     # dropped term or a wrong sign gives rate <= 1.  Pin: N + 1/2 - 0.1 <= rate <= N + 1.5.
+    print(f"N={N} rates {rates}")
     assert N + 0.4 <= rates[-1] <= N + 1.5, (errs, rates)
 
 
