@@ -95,7 +95,9 @@ def c2(scale: float = 1.0) -> Config:
 
 def c3(scale: float = 1.0) -> Config:
     n = max(4, int(round(48 * scale)))
-    m = M.kuhn_box((n, n, n), (-1, -1, -1), (1, 1, 1), bc_tag=M.BC_PASSTHROUGH)
+    # octant-mirrored Kuhn split: under the cubed-ball map the plain split puts all four
+    # vertices of some cube-corner/edge tets on the sphere (h_min / h_median 4e-4)
+    m = M.kuhn_box((n, n, n), (-1, -1, -1), (1, 1, 1), bc_tag=M.BC_PASSTHROUGH, mirror=True)
     m = M.carve_horn(M.cubed_ball(m, 1.0))
     return Config("C3", 3, m, gamma=GAMMA, pulses=[(0.10, 0.05, (-0.5, 0.0, 0.0))], steps=500, **SCALED)
 

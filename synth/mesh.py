@@ -59,8 +59,14 @@ def _hash_faces(ids: np.ndarray):
     return etoe, etof
 
 
-def kuhn_box(n, lo, hi, periodic=(False, False, False), bc_tag=BC_PASSTHROUGH) -> TetMesh:
-    """n = (nx, ny, nz) hexes on the box [lo, hi], 6 Kuhn tets per hex, hex order x fastest."""
+def kuhn_box(n, lo, hi, periodic=(False, False, False), bc_tag=BC_PASSTHROUGH, mirror=False) -> TetMesh:
+    """n = (nx, ny, nz) hexes on the box [lo, hi], 6 Kuhn tets per hex, hex order x fastest.
+
+    mirror: each hex's Kuhn diagonal is reflected per axis by the sign of its centre coordinate
+    (octant symmetry), so every tet contains the hex vertex nearest the origin.  The split stays
+    conforming (a shared face's diagonal depends only on the flips of the two axes spanning it,
+    which both hexes share).  Used under the cubed-ball map (C3), where the plain split puts
+    all four vertices of some corner/edge tets on the sphere (flat slivers)."""
     nx, ny, nz = (int(v) for v in n)
     lo, hi = np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64)
     for d, p in enumerate(periodic):
@@ -77,6 +83,10 @@ def kuhn_box(n, lo, hi, periodic=(False, False, False), bc_tag=BC_PASSTHROUGH) -
 
     k3, j3, i3 = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
     i3, j3, k3 = i3.ravel(), j3.ravel(), k3.ravel()
+    flips = np.zeros((3, i3.size), dtype=np.int64)
+    if mirror:   # reflect the local axis where the hex centre lies on the negative side
+        for d, (idx, g) in enumerate(((i3, gx), (j3, gy), (k3, gz))):
+            flips[d] = (0.5 * (g[idx] + g[idx + 1]) < -1e-12).astype(np.int64)
     tets = []
     for perm in permutations(range(3)):
         c = [np.zeros(3, dtype=np.int64)]
@@ -84,12 +94,12 @@ def kuhn_box(n, lo, hi, periodic=(False, False, False), bc_tag=BC_PASSTHROUGH) -
             nxt = c[-1].copy()
             nxt[ax] += 1
             c.append(nxt)
-        verts = [vid(i3 + o[0], j3 + o[1], k3 + o[2]) for o in c]
-        sign = np.linalg.det(np.eye(3)[list(perm)])
-        if sign < 0:                       # keep positive orientation
-            verts[1], verts[2] = verts[2], verts[1]
+        verts = [vid(i3 + (o[0] ^ flips[0]), j3 + (o[1] ^ flips[1]), k3 + (o[2] ^ flips[2])) for o in c]
         tets.append(np.stack(verts, axis=1))
     etov = np.stack(tets, axis=1).reshape(-1, 4).astype(np.int64)   # hex-major, 6 per hex
+    v = vxyz[etov]                                                   # keep positive orientation
+    neg = np.linalg.det(np.stack([v[:, 1] - v[:, 0], v[:, 2] - v[:, 0], v[:, 3] - v[:, 0]], axis=1)) < 0
+    etov[neg, 1], etov[neg, 2] = etov[neg, 2].copy(), etov[neg, 1].copy()
 
     # periodic identification for hashing only (coordinates stay unwrapped)
     iv = np.arange(nx + 1)
@@ -224,3 +234,39 @@ def face_orientation_codes(mesh: TetMesh, part=None):
             sig = tuple(int(j) for j in d.argmin(axis=1))
             codes.add((f, f2, sig))
     return codes
+
+
+def quality(mesh: TetMesh) -> dict:
+    """Mesh-quality statistics for the input recipe (SURVEY §7 hard part 7): J = det of the
+    affine map from the reference tet (volume 4/3), h = 3 V / max face area, min and
+    median, and the minimum dihedral angle in degrees."""
+    v = mesh.vxyz[mesh.etov]                                          # (K, 4, 3)
+    e1, e2, e3 = v[:, 1] - v[:, 0], v[:, 2] - v[:, 0], v[:, 3] - v[:, 0]
+    J = np.einsum("kd,kd->k", e1, np.cross(e2, e3)) / 8.0
+    vol = np.abs(J) * 8.0 / 6.0
+    areas = []
+    normals = []
+    for f in FACES:
+        a, b, c = v[:, f[0]], v[:, f[1]], v[:, f[2]]
+        nrm = np.cross(b - a, c - a)
+        areas.append(0.5 * np.linalg.norm(nrm, axis=1))
+        normals.append(nrm / np.linalg.norm(nrm, axis=1)[:, None])
+    areas = np.stack(areas, axis=1)
+    h = 3.0 * vol / areas.max(axis=1)
+    # dihedral angle along the edge shared by faces i and j: pi - angle between outward normals
+    opp = OPPOSITE
+    cen = v.mean(axis=1)
+    out = []
+    for f, nrm in enumerate(normals):
+        fc = v[:, FACES[f]].mean(axis=1)
+        sgn = np.sign(np.einsum("kd,kd->k", nrm, fc - cen))
+        out.append(nrm * sgn[:, None])
+    dmin = np.full(mesh.K, np.pi)
+    for i in range(4):
+        for j in range(i + 1, 4):
+            cosang = np.clip(np.einsum("kd,kd->k", out[i], out[j]), -1, 1)
+            dmin = np.minimum(dmin, np.pi - np.arccos(cosang))
+    return {"K": int(mesh.K), "J_min": float(J.min()), "J_median": float(np.median(J)),
+            "h_min": float(h.min()), "h_median": float(np.median(h)),
+            "h_min_over_median": float(h.min() / np.median(h)),
+            "min_dihedral_deg": float(np.degrees(dmin.min())), "median_min_dihedral_deg": float(np.degrees(np.median(dmin)))}
