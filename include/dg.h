@@ -156,6 +156,16 @@ dg_status dg_rk_step(dg_ctx* ctx, double dt, int nsteps, void* stream);
  * (e.g. the NCCL halo kernels, see dg_rk_step).  Results do not depend on it. */
 dg_status dg_set_max_ctas(dg_ctx* ctx, int max_ctas);
 
+/* One-sided amplitude spectra of m uniformly sampled pressure records (SURVEY §8(f) N4,
+ * DESIGN.md reading A22; Fig. 5 and §3): per record the mean is removed,
+ * X_k = sum_j x_j e^{-2 pi i jk/n}, amp_k = 2|X_k|/n (|X_k|/n at k = 0 and, for even n, at
+ * k = n/2), db_k = 20 log10(amp_k) floored at -200 dB (re 1 scaled pressure unit).
+ * x: DEVICE array n x m row-major (sample j of record r at x[j*m + r], e.g. a
+ * dg_sensors_record buffer column); amp, db: DEVICE arrays (n/2+1) x m, caller-owned.
+ * Stream-ordered on `stream`; no ctx (errors via dg_last_error(NULL)): DG_EARG for NULL
+ * pointers, n < 2, m < 1 or m > 65535; DG_ECUDA on a launch failure. */
+dg_status dg_spectrum(const double* x, int64_t n, int64_t m, double* amp, double* db, void* stream);
+
 /* Compile-time configuration of this build ("key=value;..."), for benchmark records. */
 const char* dg_build_info(void);
 
@@ -171,8 +181,15 @@ dg_status dg_stable_dt(dg_ctx* ctx, double cfl, double* dt, void* stream);
 /* ---- multi-GPU (element partition) ------------------------- */
 /* NCCL unique id (128 bytes) for rank 0 to broadcast. */
 dg_status dg_nccl_get_unique_id(void* out128);
-/* Initialise this ctx's NCCL communicator (nranks must equal desc->nparts). */
+/* Initialise this ctx's NCCL communicator (nranks must equal desc->nparts).  The communicator
+ * is created with maxCTAs = the dg_set_nccl_ctas value (default 2) and a highest-priority
+ * stream; while the halo is in flight the interior stage launch of dg_rk_step / dg_rhs
+ * leaves that many SMs free, so the exchange overlaps the interior work (
+ * DG needs only face-neighbour data).  DG_ENCCL on an NCCL failure. */
 dg_status dg_comm_init(dg_ctx* ctx, const void* unique_id128, int nranks);
+/* SMs reserved for NCCL's kernel during the interior launch (0 = none: the halo kernel then
+ * waits for free SMs); must precede dg_comm_init, nctas in [0, 64], else DG_EARG / DG_ESTATE. */
+dg_status dg_set_nccl_ctas(dg_ctx* ctx, int nctas);
 
 /* Halo description for transport-agnostic use (tests, custom transports):
  * per peer p in [0, npeers): its rank, and the face-trace records sent to and

@@ -32,7 +32,8 @@ SYMBOLS = (
     "dg_halo_buffers", "dg_halo_records", "dg_stage_pack", "dg_stage_compute", "dg_stage_finish", "dg_rhs_compute",
     "dg_get_operators", "dg_get_maps", "dg_get_geometry", "dg_launch_count",
     "dg_sensors_set", "dg_sensors_sample", "dg_sensors_record", "dg_sensors_recorded",
-    "dg_set_max_ctas", "dg_build_info", "dg_halo_exchange",
+    "dg_set_max_ctas", "dg_build_info", "dg_halo_exchange", "dg_set_nccl_ctas",
+    "dg_spectrum",
 )
 
 
@@ -108,6 +109,8 @@ def _load():
         "dg_sensors_record": (I, [P, P, I64]),
         "dg_sensors_recorded": (I64, [P]),
         "dg_set_max_ctas": (I, [P, I]),
+        "dg_set_nccl_ctas": (I, [P, I]),
+        "dg_spectrum": (I, [P, C.c_int64, C.c_int64, P, P, P]),
         "dg_build_info": (C.c_char_p, []),
         "dg_halo_exchange": (I, [P, P]),
     }
@@ -247,6 +250,14 @@ def dg_rk_step(ctx, dt: float, nsteps: int, stream: int):
 
 def dg_set_max_ctas(ctx, max_ctas: int):
     _check(_lib.dg_set_max_ctas(ctx, int(max_ctas)), ctx)
+
+
+def dg_set_nccl_ctas(ctx, nctas: int):
+    _check(_lib.dg_set_nccl_ctas(ctx, int(nctas)), ctx)
+
+
+def dg_spectrum(x_ptr: int, n: int, m: int, amp_ptr: int, db_ptr: int, stream: int):
+    _check(_lib.dg_spectrum(x_ptr, int(n), int(m), amp_ptr, db_ptr, stream), None)
 
 
 def dg_build_info() -> str:

@@ -12,6 +12,7 @@
 
 #include "ctx.h"
 #include "kernels.cuh"
+#include "spectrum.cuh"
 
 namespace {
 
@@ -257,6 +258,18 @@ dg_status halo_exchange(dg_ctx* c, cudaStream_t st) {
   return DG_OK;
 }
 
+// grid cap of a launch: the interior launch of a partitioned step (which == 1, halo in flight)
+// leaves nccl_ctas SMs free, so NCCL's send/recv kernel runs beside it instead of queueing
+// behind the persistent CTAs (they hold every SM's registers and shared memory until they finish)
+int launch_cap(const dg_ctx* c, int which) {
+  int cap = c->max_ctas;
+  if (which == 1 && c->comm && c->nccl_ctas > 0) {
+    const int free_cap = std::max(1, num_sms() - c->nccl_ctas);
+    cap = cap > 0 ? std::min(cap, free_cap) : free_cap;
+  }
+  return cap;
+}
+
 dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st) {
   double a, b, cc;
   coeffs(c, s, a, b, cc);
@@ -266,8 +279,9 @@ dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st)
   A.dt = dt;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, c->max_ctas, st)
-                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, c->max_ctas, st));
+    const int cap = launch_cap(c, which);
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, cap, st)
+                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, cap, st));
     ++c->launches;
   }
   return DG_OK;
@@ -477,6 +491,25 @@ dg_status dg_get_time(const dg_ctx* c, double* t) {
   return DG_OK;
 }
 
+dg_status dg_spectrum(const double* x, int64_t n, int64_t m, double* amp, double* db, void* stream) {
+  if (!x || !amp || !db) return set_err(nullptr, DG_EARG, "dg_spectrum: NULL pointer");
+  if (n < 2 || m < 1 || m > 65535) return set_err(nullptr, DG_EARG, "dg_spectrum: need n >= 2 and 1 <= m <= 65535");
+  const int64_t nb = n / 2 + 1;
+  const int wpb = 8;
+  const dim3 grid(unsigned((nb + wpb - 1) / wpb), unsigned(m));
+  dgk::spectrum_kernel<<<grid, 32 * wpb, 0, static_cast<cudaStream_t>(stream)>>>(x, n, m, amp, db);
+  CUDA_TRY(nullptr, cudaGetLastError());
+  return DG_OK;
+}
+
+dg_status dg_set_nccl_ctas(dg_ctx* c, int nctas) {
+  if (!c) return set_err(c, DG_EARG, "ctx is NULL");
+  if (nctas < 0 || nctas > 64) return set_err(c, DG_EARG, "nctas must be in [0, 64]");
+  if (c->comm) return set_err(c, DG_ESTATE, "dg_set_nccl_ctas must precede dg_comm_init");
+  c->nccl_ctas = nctas;
+  return DG_OK;
+}
+
 dg_status dg_set_max_ctas(dg_ctx* c, int max_ctas) {
   if (!c) return set_err(nullptr, DG_EARG, "ctx is NULL");
   if (max_ctas < 0) return set_err(c, DG_EARG, "max_ctas must be >= 0");
@@ -549,8 +582,8 @@ dg_status dg_rhs_compute(dg_ctx* c, double t, double* out, int which, void* stre
   A.out = out;
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
-    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, c->max_ctas, st)
-                                             : launch_stage<dgk::MODE_RHS>(c->N, A, c->max_ctas, st));
+    CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, launch_cap(c, which), st)
+                                             : launch_stage<dgk::MODE_RHS>(c->N, A, launch_cap(c, which), st));
     ++c->launches;
   }
   return DG_OK;
@@ -745,10 +778,20 @@ dg_status dg_comm_init(dg_ctx* c, const void* uid, int nranks) {
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
   ncclComm_t comm;
-  NCCL_TRY(c, ncclCommInitRank(&comm, nranks, id, c->rank));
+  // NCCL's kernels are capped at DG_NCCL_CTAS (default 2) CTAs; the interior stage launch leaves
+  // that many SMs free (launch_cap), and the communication stream has the highest priority
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  const int nctas = c->nccl_ctas;   // dg_set_nccl_ctas, default 2
+  if (nctas > 0) {
+    cfg.minCTAs = 1;
+    cfg.maxCTAs = nctas;
+  }
+  NCCL_TRY(c, ncclCommInitRankConfig(&comm, nranks, id, c->rank, &cfg));
   c->comm = comm;
   cudaStream_t cs;
-  CUDA_TRY(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CUDA_TRY(c, cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
   c->comm_stream = cs;
   cudaEvent_t e1, e2;
   CUDA_TRY(c, cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));

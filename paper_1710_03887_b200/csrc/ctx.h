@@ -24,6 +24,7 @@ struct dg_ctx {
   double pref = 0.0;              // ambient pressure p(q_inf) subtracted from the fluxes (A14), 0 if unused
   bool qinf_valid = false;
   int max_ctas = 0;               // stage-kernel grid cap (0 = one CTA per SM)
+  int nccl_ctas = 2;              // SMs left free for NCCL's kernel while the interior launch runs (P > 1)
   int scheme = DG_SCHEME_NODAL;
   dgb::RefElem ref;
   dgb::ModalTables modal;           // scheme == DG_SCHEME_MODAL

@@ -307,7 +307,16 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
   if DG_SKIPQ(2) return;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+  // DG_F1 (default): the own trace is read from shared memory once -- the first pass keeps
+  // q+ - q- and n.F(q-) - n.F(q+) (10 values per pass, as many as the primitives it replaced),
+  // the second pass only applies the face max
+#ifndef DG_F1
+#define DG_F1 2
+#endif
+  // (N = 4: 8 B of spills, still C4 54.3 -> 55.7 GDOF/s; C3 59.6 -> 60.3)
+  constexpr bool F1 = DG_F1 == 2 || (DG_F1 == 1 && N <= 3);
   double rip[NPASS], unp[NPASS], pp[NPASS], lam[NPASS], unmv[NPASS], pmv[NPASS];
+  double dqv[F1 ? NPASS : 1][5], gfv[F1 ? NPASS : 1][5];
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
@@ -328,18 +337,64 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
     pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
     const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
     lam[u] = act ? l : 0.0;
+    if constexpr (F1) {
+      const double dp = pm - pp[u];
+      gfv[u][0] = fma(qm0, unm, -qp[u][0] * unp[u]);
+      gfv[u][1] = fma(dp, nx, fma(qm1, unm, -qp[u][1] * unp[u]));
+      gfv[u][2] = fma(dp, ny, fma(qm2, unm, -qp[u][2] * unp[u]));
+      gfv[u][3] = fma(dp, nz, fma(qm3, unm, -qp[u][3] * unp[u]));
+      gfv[u][4] = fma(qm4 + pm, unm, -(qp[u][4] + pp[u]) * unp[u]);
+      dqv[u][0] = qp[u][0] - qm0;
+      dqv[u][1] = qp[u][1] - qm1;
+      dqv[u][2] = qp[u][2] - qm2;
+      dqv[u][3] = qp[u][3] - qm3;
+      dqv[u][4] = qp[u][4] - qm4;
+    }
   }
   if (A.lambda_mode == 0) {
+    if constexpr ((SEGW & (SEGW - 1)) == 0) {
 #pragma unroll
-    for (int d = 1; d < SEGW; d <<= 1) {
+      for (int d = 1; d < SEGW; d <<= 1) {
 #pragma unroll
-      for (int u = 0; u < NPASS; ++u) {
-        const long long a = __double_as_longlong(lam[u]);
-        const long long o = __shfl_xor_sync(0xffffffffu, a, d);
-        lam[u] = __longlong_as_double(a > o ? a : o);
+        for (int u = 0; u < NPASS; ++u) {
+          const long long a = __double_as_longlong(lam[u]);
+          const long long o = __shfl_xor_sync(0xffffffffu, a, d);
+          lam[u] = __longlong_as_double(a > o ? a : o);
+        }
+      }
+    } else {
+      // segments of SEGW = Nfp lanes (not a power of two): cyclic rotations within the segment,
+      // the window doubling each step (1, 2, 4, 8 ... >= Nfp); lanes outside a segment read themselves
+      const int lane = threadIdx.x & 31;
+      const int sb = lane - i;
+#pragma unroll
+      for (int d = 1; d < SEGW; d <<= 1) {
+        const int src = lane_ok ? sb + (i + d) % SEGW : lane;
+#pragma unroll
+        for (int u = 0; u < NPASS; ++u) {
+          const long long a = __double_as_longlong(lam[u]);
+          const long long o = __shfl_sync(0xffffffffu, a, src);
+          lam[u] = __longlong_as_double(a > o ? a : o);
+        }
       }
     }
   }
+  if constexpr (F1) {
+#pragma unroll
+    for (int u = 0; u < NPASS; ++u) {
+      const int face = fbase + u * fstride;
+      const bool slot = lane_ok && face < flim;
+      const bool act = slot && (face >> 2) < ne;
+      const int fc = slot ? face : 0;
+      const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+      const double hfs = act ? 0.5 * g_s[e * GEO + 9 + 4 * f + 3] : 0.0;
+      double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
+      if (slot) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam[u], dqv[u][c], gfv[u][c]) : 0.0;
+      }
+    }
+  } else {
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
@@ -365,6 +420,7 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
 #pragma unroll
       for (int c = 0; c < 5; ++c) xd[c * XSF] = act ? hfs * fma(lam[u], qp[u][c] - qm[c], df[c]) : 0.0;
     }
+  }
   }
 }
 
@@ -392,12 +448,25 @@ struct WS {
   static constexpr int ROWS = 5 * EB;                       // multiple of 8 (DMMA m8 row tiles)
   static_assert(ROWS % 8 == 0, "rows must fill DMMA m8 tiles");
   // faces per producer warp-pass: one face per power-of-two lane segment (butterfly face max)
-  static constexpr int SEGW = Shape<N>::NFP <= 4 ? 4 : Shape<N>::NFP <= 8 ? 8 : Shape<N>::NFP <= 16 ? 16 : 32;
+  // N = 3: dense segments of Nfp = 10 lanes (3 faces per warp pass, 2 passes instead of 3 with
+  // 16-lane segments: a third fewer face-term instructions); face max by rotations
+#ifndef DG_FDENSE
+#define DG_FDENSE 1
+#endif
+  static constexpr bool FDENSE = DG_FDENSE && N == 3;
+  static constexpr int SEGW = FDENSE ? Shape<N>::NFP
+                              : Shape<N>::NFP <= 4 ? 4 : Shape<N>::NFP <= 8 ? 8 : Shape<N>::NFP <= 16 ? 16 : 32;
   static constexpr int NSEG = 32 / SEGW;
   static constexpr int FPASS = (4 * EB + PW * NSEG - 1) / (PW * NSEG);   // face passes per producer warp
   // X is split into its volume block [ROWS][XSV] and face block [ROWS][XSF];
   // strides == 12 (mod 16) doubles keep the A-fragment loads conflict-free
-  static constexpr int XSV = (Shape<N>::KVP + 3) / 16 * 16 + 12;
+  // when Np == 4 (mod 16) (N = 1, 3), XSV == 4 (mod 16) also makes consecutive elements' volume
+  // rows continue each other's bank sequence (5 XSV == Np mod 16): conflict-free flux stores
+#ifndef DG_XSV4
+#define DG_XSV4 1
+#endif
+  static constexpr bool XS4 = DG_XSV4 && Shape<N>::NP % 16 == 4;
+  static constexpr int XSV = XS4 ? (Shape<N>::KVP + 11) / 16 * 16 + 4 : (Shape<N>::KVP + 3) / 16 * 16 + 12;
   static constexpr int XSF = (4 * Shape<N>::NFP + 3) / 16 * 16 + 12;
   // B operand in shared memory, per k-step: NPG n-tile pairs (64 doubles, a lane's two values
   // adjacent) then, if NTL is odd, the trailing n-tile compacted to the lanes of its GS real
@@ -461,39 +530,83 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0)
                : "d"(a0), "d"(b0));
 }
 
-// Balanced work split for the consumers: units are (8-row tile, n-tile pair) (weight 2) and
-// (8-row tile, odd trailing n-tile) (weight 1).  Pairs go round-robin over the consumer warps,
-// singles greedily to the least-loaded SMSP (warp cw runs on SMSP cw % 4); every consumer
-// thread evaluates the same deterministic assignment.
+// Balanced work split for the consumers: units are (8-row tile, n-tile pair) and (8-row tile,
+// odd trailing n-tile).  Pairs go round-robin over the consumer warps; singles are placed one at
+// a time on the warp minimising (its SMSP's load, its own load) -- warp cw runs on SMSP cw % 4 --
+// in FP64-pipe cycles per k-step: a pair 32 (two DMMA), a single 2 GS on DFMA (16 as a DMMA),
+// plus, for a warp's first single, DG_SBV (the per-k-step B loads of the odd tile, which every
+// warp holding singles repeats; 4 by default, so singles gather on few warps).  The plan is a
+// compile-time constant every consumer thread reads.
+#ifndef DG_SBV
+#define DG_SBV 0
+#endif
 template <int N>
 struct M8Plan {
   static constexpr int MT8 = WS<N>::ROWS / 8;
   static constexpr int NPG = WS<N>::NPG, HS = WS<N>::HS;
   static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N>::CW;
   static constexpr int CPMAX = (P + CW - 1) / CW;
-  static constexpr int CSMAX = 4;   // dispatch bound on singles per warp
+  static constexpr bool SDF1 = WS<N>::GS > 0 && WS<N>::GS <= 4;
+#ifdef DG_SWSI
+  static constexpr int WSI = DG_SWSI;
+#else
+  static constexpr int WSI = 16;   // pipe-exact 2 GS concentrates singles: C3 56.9 vs 61.8 GDOF/s
+#endif
+  static constexpr int SBV = P > 0 ? DG_SBV : 0;   // singles only (N = 1): spread them
+  struct Owners {
+    int w[SG > 0 ? SG : 1];
+  };
+  static constexpr Owners owners() {
+    Owners o{};
+    int load[CW] = {}, smsp[4] = {}, ns[CW] = {};
+    for (int w = 0; w < CW; ++w) {
+      load[w] = 32 * (P > w ? (P - 1 - w) / CW + 1 : 0);
+      smsp[w % 4] += load[w];
+    }
+    for (int s = 0; s < SG; ++s) {
+      int best = 0;
+      for (int w = 1; w < CW; ++w) {
+        const int cb = WSI + (ns[best] ? 0 : SBV), cc = WSI + (ns[w] ? 0 : SBV);
+        // with a B-load term, ties go to a warp that already loads the odd tile's B values
+        const int a = ((smsp[w % 4] + cc) * 4096 + load[w] + cc) * 2 + (SBV > 0 && ns[w] == 0);
+        const int b = ((smsp[best % 4] + cb) * 4096 + load[best] + cb) * 2 + (SBV > 0 && ns[best] == 0);
+        if (a < b) best = w;
+      }
+      const int c = WSI + (ns[best] ? 0 : SBV);
+      load[best] += c;
+      smsp[best % 4] += c;
+      ++ns[best];
+      o.w[s] = best;
+    }
+    return o;
+  }
+  static constexpr int count(int w) {
+    int n = 0;
+    for (int s = 0; s < SG; ++s) n += owners().w[s] == w;
+    return n;
+  }
+  static constexpr int maxcount() {
+    int m = 0;
+    for (int w = 0; w < CW; ++w) m = count(w) > m ? count(w) : m;
+    return m;
+  }
+  static constexpr int CSMAX = maxcount() > 0 ? maxcount() : 1;
+  static constexpr int npairs(int w) { return P > w ? (P - 1 - w) / CW + 1 : 0; }
+  static constexpr bool occurs(int pa, int si) {
+    for (int w = 0; w < CW; ++w)
+      if (npairs(w) == pa && count(w) == si) return true;
+    return false;
+  }
 };
 
 template <int N>
 __device__ __forceinline__ void m8_singles(int cw, int* out, int& count) {
   using PL = M8Plan<N>;
-  int load[PL::CW];
-  int smsp[4] = {0, 0, 0, 0};
-  for (int w = 0; w < PL::CW; ++w) {
-    load[w] = 2 * (PL::P > w ? (PL::P - 1 - w) / PL::CW + 1 : 0);
-    smsp[w % 4] += load[w];
-  }
+  constexpr typename PL::Owners o = PL::owners();
   count = 0;
-  for (int s = 0; s < PL::SG; ++s) {
-    int best = 0;
-    for (int w = 1; w < PL::CW; ++w) {
-      const int a = smsp[w % 4] * 64 + load[w], b = smsp[best % 4] * 64 + load[best];
-      if (a < b) best = w;
-    }
-    load[best] += 1;
-    smsp[best % 4] += 1;
-    if (best == cw && count < PL::CSMAX) out[count++] = s;
-  }
+#pragma unroll
+  for (int s = 0; s < PL::SG; ++s)
+    if (o.w[s] == cw) out[count++] = s;
 }
 
 // Consumer warp: DMMA m8n8k4 over its units, then the LSERK epilogue.  Full tiles run the
@@ -552,6 +665,14 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     tma_load_1d(ib + W::BQ + W::BG, A.nbr + size_t(e0) * 4, W::BN, io.barIn + b);
     tma_load_1d(ib + W::BQ + W::BG + W::BN, A.code + size_t(e0) * 4, W::BC, io.barIn + b);
   };
+  // DG_EPI=1 (experiment): the epilogue stores res and Q_new straight from registers to global
+  // memory; nothing is written back to shared memory, so no consumer barrier and no bulk store
+  // close the tile.  The tile's shared buffers (input, residual) are released one tile later,
+  // after the next XV_FULL barrier, which every consumer warp passes only after its epilogue.
+#ifndef DG_EPI   // measured slower: C4 50.7 vs 55.6, C3 60.6 vs 61.4 GDOF/s (uncoalesced row-fragment stores)
+#define DG_EPI 0
+#endif
+  constexpr bool EPI = DG_EPI && MODE == MODE_UPDATE;
   if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
@@ -619,7 +740,22 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 0);
     nbar_sync(W::BAR_XV_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 1);
-    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
+    if (EPI) {
+      // every consumer warp has finished tile j-1's epilogue (it passed XV_FULL after it): its
+      // input and residual buffers are free
+      if (io.ctid == IOT) {
+        if (W::NRES == 1 && j >= 1 && ne == EB) load_res(j);
+        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) load_res(j + 1);
+        if (W::NIN == 2 && j >= 1 && j + 1 < io.nmine && tile_full(j + 1)) fetch_in(j + 1);
+      }
+      if ((io.ctid >> 5) == IOW && j >= 1) {
+        const int pbuf = (j - 1) % W::NIN;
+        if ((W::NIN == 2 && j + 1 < io.nmine && !tile_full(j + 1)) || (W::NIN > 2 && j - 1 + W::NIN < io.nmine)) {
+          __syncwarp();
+          nbar_arrive(W::BAR_Q_EMPTY + pbuf, W::PT + 32);
+        }
+      }
+    } else if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
       // tile j-1's residual store has left sRes by now (issued at the end of its epilogue)
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       load_res(j);
@@ -675,8 +811,14 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             const int li = (unit_mt(u) * 8 + g) * NP + n;   // == (e*5 + c)*NP + n
             const double rr = fma(A.a, rv[u - u0][q], A.dt * acc[u][q]);
             const double qn = fma(A.b, rr, qv[u - u0][q]);
-            sRes[li] = rr;
-            q_s[li] = qn;
+            if (EPI) {
+              const size_t gi = size_t(e0) * 5 * NP + li;
+              A.res[gi] = rr;
+              A.Qout[gi] = qn;
+            } else {
+              sRes[li] = rr;
+              q_s[li] = qn;
+            }
           }
       }
     } else {
@@ -703,6 +845,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       }
     }
     if (io.ctid < 32) trace_ev(A, j, 6);
+    if (EPI) continue;   // buffers are released after the next XV_FULL (above)
     if (staged) {
       // every thread that wrote the staged tiles orders its generic-proxy stores before the
       // async-proxy (TMA) reads of the bulk stores issued after the barrier
@@ -836,7 +979,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // ---- issue this pwarp's neighbour-trace gathers for the whole tile first: their latency
       //      hides behind the volume phase
       const int seg = lane / W::SEGW, i = lane - seg * W::SEGW;
-      const bool lane_ok = i < NFP;
+      const bool lane_ok = i < NFP && seg < W::NSEG;
       const int fbase = pwarp * W::NSEG + seg;
       double qp[W::FPASS][5];
       face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
@@ -928,15 +1071,18 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
     constexpr int CP = PL::CPMAX, CPm = PL::CPMAX > 0 ? PL::CPMAX - 1 : 0;
     // instantiate only the per-warp shapes the greedy plan can produce
-    constexpr int SMAX = (PL::SG + PL::CW - 1) / PL::CW + 1;
+    constexpr int SMAX = PL::maxcount();
 #define DG_M8_CASE(PA, SI)                                                   \
-  if constexpr (SI <= SMAX) {                                                \
+  if constexpr (PL::occurs(PA, SI)) {                                        \
     if (np8 == PA && ns == SI) ws_consumer_m8<N, MODE, PA, SI>(io, cw, singles); \
   }
     DG_M8_CASE(CP, 0) DG_M8_CASE(CP, 1) DG_M8_CASE(CP, 2) DG_M8_CASE(CP, 3) DG_M8_CASE(CP, 4)
+    DG_M8_CASE(CP, 5) DG_M8_CASE(CP, 6) DG_M8_CASE(CP, 7) DG_M8_CASE(CP, 8)
     if (CPm != CP) {
       DG_M8_CASE(CPm, 0) DG_M8_CASE(CPm, 1) DG_M8_CASE(CPm, 2) DG_M8_CASE(CPm, 3) DG_M8_CASE(CPm, 4)
+      DG_M8_CASE(CPm, 5) DG_M8_CASE(CPm, 6) DG_M8_CASE(CPm, 7) DG_M8_CASE(CPm, 8)
     }
+    static_assert(SMAX <= 8, "singles per warp beyond the dispatch cases");
 #undef DG_M8_CASE
   }
 }
