@@ -115,6 +115,16 @@ __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   }
 }
 
+// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*2 + k, tiles < 48
+__device__ __forceinline__ void trace_w(const StageArgs& A, int j, int k) {
+  if (DG_TRACE && blockIdx.x == 0 && j < 48 && A.trace) {
+    __syncwarp();
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 2 + k] = t;
+  }
+}
+
 // rho > 0, p > 0 and all five conserved values finite, decided with integer ops on the
 // IEEE bit patterns (keeps the check off the FP64 pipe)
 __device__ __forceinline__ bool state_ok(double rho, double p, double mx, double my, double mz, double E) {
@@ -271,6 +281,56 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
                                             const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
                                             const uint8_t* sFm, double (&qp)[NPASS][5]) {
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
+  // DG_GATHER2 (default: N <= 3; C3 61.7 -> 64.1, C2 52.0 -> 53.2 GDOF/s; at N = 4 55.6 -> 52.4)
+#ifndef DG_GATHER2
+#define DG_GATHER2 1
+#endif
+  if constexpr (DG_GATHER2 == 2 || (DG_GATHER2 == 1 && N <= 3)) {
+    // all passes' shared-memory lookups level by level (code and neighbour, then the node
+    // table), so the passes' dependent load chains overlap instead of running one after another
+    int code[NPASS], nb[NPASS], node[NPASS];
+    bool ok[NPASS];
+#pragma unroll
+    for (int u = 0; u < NPASS; ++u) {
+      const int face = fbase + u * fstride;
+      const int e = face >> 2, f = face & 3;
+      ok[u] = !DG_SKIPQ(2) && lane_ok && face < flim && e < ne;
+      const int ec = ok[u] ? e : 0;
+      code[u] = ok[u] ? int(c_s[ec * 4 + f]) : CODE_BC;
+      nb[u] = n_s[ec * 4 + f];
+    }
+#pragma unroll
+    for (int u = 0; u < NPASS; ++u) {
+      const int f = (fbase + u * fstride) & 3;
+      const int ii = lane_ok ? i : 0;
+      node[u] = code[u] < CODE_GHOST ? int(sTbl[(f * 24 + code[u]) * NFP + ii])
+                : code[u] < CODE_BC ? int(sTblf[(f * 24 + code[u] - CODE_GHOST) * NFP + ii]) : int(sFm[f * NFP + ii]);
+    }
+#pragma unroll
+    for (int u = 0; u < NPASS; ++u) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
+      if (code[u] < CODE_GHOST) {
+        const double* q2 = A.Qin + size_t(nb[u]) * 5 * NP + node[u];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[u][c] = __ldg(q2 + c * NP);
+      } else if (code[u] < CODE_BC) {
+        const double* q2 = A.recv + size_t(nb[u]) * 5 * NFP + node[u];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[u][c] = __ldg(q2 + c * NFP);
+      } else if (ok[u]) {   // boundary ghost from the own trace (Q of this tile is in shared memory)
+        const int face = fbase + u * fstride;
+        const int e = face >> 2, f = face & 3;
+        const double* G = g_s + e * GEO + 9 + 4 * f;
+        const double* q = q_s + e * 5 * NP + node[u];
+        double qm[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qm[c] = q[c * NP];
+        ghost_trace(A, code[u] - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
@@ -424,6 +484,46 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
   }
 }
 
+// Pointwise volume flux of node slot idx of a tile (Eq. 1-2): contravariant fluxes
+// Ft_d = xi_d,x F + xi_d,y G + xi_d,z H (d = r, s, t) into the volume block of X, row (e, field),
+// column d Np + n; slots past the tile's nodes compute on a clamped node and store zeros (or
+// nothing past the tile), so the loop around it can stay branch-free.
+template <int N, int XSV>
+__device__ __forceinline__ void vol_node(const StageArgs& A, int idx, const double* q_s, const double* g_s, int e0,
+                                         int ne, double gm1, double* sXv, int ebn) {
+  constexpr int NP = Shape<N>::NP;
+  const bool inb = idx < ebn;
+  const int ic = inb ? idx : 0;
+  const int e = ic / NP, n = ic - e * NP;
+  const bool act = inb && e < ne;
+  const double* q = q_s + e * 5 * NP + n;
+  const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
+  const double ri = rcp_nr(rho);
+  const double u = mx * ri, v = my * ri, w = mz * ri;
+  const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
+  if (act && !state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
+  const double* G = g_s + e * GEO;
+  const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
+  double f[3][5];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
+    const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
+    f[d][0] = rho * U;
+    f[d][1] = fma(cx, pd, mx * U);
+    f[d][2] = fma(cy, pd, my * U);
+    f[d][3] = fma(cz, pd, mz * U);
+    f[d][4] = Ep * U;
+  }
+  if (inb) {
+    double* xr = sXv + (e * 5) * XSV + n;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int c = 0; c < 5; ++c) xr[c * XSV + d * NP] = act ? f[d][c] : 0.0;
+  }
+}
+
 template <int N>
 struct WS {
 #ifdef DG_WS_EB
@@ -433,17 +533,33 @@ struct WS {
 #endif
   // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 3 the
   // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3)
+  // DG_SMR: 20 warps (12 producer + 8 consumer) with the register file re-split at run time
+  // (setmaxnreg): the kernel is compiled for R0 = 65536 / NT registers, consumer warps drop to
+  // CREG and producer warps rise to PREG, with CW (R0 - CREG) >= PW (PREG - R0) so the
+  // increase is served by the decrease
+#ifndef DG_SMR
+#define DG_SMR 0
+#endif
+  static constexpr bool SMR = DG_SMR && N >= 3;
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;
 #else
-  static constexpr int PW = N == 3 ? 12 : 8;
+  static constexpr int PW = SMR ? 12 : N == 3 ? 12 : 8;
 #endif
 #ifdef DG_WS_CW
   static constexpr int CW = DG_WS_CW;
 #else
-  static constexpr int CW = N == 3 ? 4 : 8;
+  static constexpr int CW = SMR ? 8 : N == 3 ? 4 : 8;
 #endif
   static constexpr int NT = 32 * (PW + CW);
+  static constexpr int R0 = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
+#ifdef DG_SMR_CREG
+  static constexpr int CREG = DG_SMR_CREG;
+#else
+  static constexpr int CREG = 72;
+#endif
+  static constexpr int PREG = R0 + (CW * (R0 - CREG) / PW) / 8 * 8;
+  static_assert(!SMR || (CW % 4 == 0 && PW % 4 == 0 && PREG >= R0 && PREG <= 248 && CREG >= 24), "register split");
   static constexpr int PT = 32 * PW, CT = 32 * CW;
   static constexpr int ROWS = 5 * EB;                       // multiple of 8 (DMMA m8 row tiles)
   static_assert(ROWS % 8 == 0, "rows must fill DMMA m8 tiles");
@@ -497,7 +613,17 @@ struct WS {
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
   static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
-                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9;
+                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9, BAR_CV = 10;
+  // DG_CTAIL (N = 4): the volume slots of the last, partial producer round (EB Np - (VR-1) PT
+  // = 48 nodes at N = 4) are computed by the two last consumer warps for the next tile, right
+  // after their volume contraction, so the producers' serial volume phase is one round shorter
+#ifndef DG_CTAIL   // measured slower: C4 53.3 vs 55.6 GDOF/s (the two-round volume phase took as long)
+#define DG_CTAIL 0
+#endif
+  static constexpr int VR = (EB * Shape<N>::NP + PT - 1) / PT;
+  static constexpr int TAILN = EB * Shape<N>::NP - (VR - 1) * PT;
+  static constexpr bool CTAIL = DG_CTAIL && N == 4 && VR >= 2 && TAILN > 0 && TAILN <= 64 && CW >= 2;
+  static constexpr int CT0 = (CW - 2) * 32;   // first consumer thread of the tail
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -762,12 +888,28 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
     kloop(KBlk<XSV, 0, S::KSV>{});
     if (io.ctid < 32) trace_ev(A, j, 2);
-    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+    if constexpr (W::CTAIL) {
+      if (j + 1 < io.nmine) {
+        nbar_sync(W::BAR_CV, W::CT);   // every consumer warp is done reading Xv(j)
+        nbar_arrive(W::BAR_XV_EMPTY, NT);
+        if (io.ctid >= W::CT0 && io.ctid < W::CT0 + W::TAILN && tile_full(j + 1)) {
+          const int b1 = (j + 1) % W::NIN;
+          mbar_wait(io.barIn + b1, ((j + 1) / W::NIN) & 1);
+          const unsigned char* ib = io.in0 + b1 * W::BIN;
+          vol_node<N, XSV>(A, (W::VR - 1) * W::PT + io.ctid - W::CT0, reinterpret_cast<const double*>(ib),
+                           reinterpret_cast<const double*>(ib + W::BQ), e0 + EB * int(gridDim.x), EB, A.gamma - 1.0,
+                           io.sXv, EB * NP);
+        }
+      }
+    } else {
+      if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
+    }
 
     nbar_sync(W::BAR_XF_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 3);
     kloop(KBlk<XSF, S::KSV, S::KS4>{});
     if (io.ctid < 32) trace_ev(A, j, 4);
+    trace_w(A, j, 0);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
     if (SDF) {   // sum the singles' partial products over the 4 lanes of a row; lane t keeps column t
 #pragma unroll
@@ -785,7 +927,6 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
     const bool staged = MODE == MODE_UPDATE && ne == EB;
     if (staged) mbar_wait(io.barRes + j % W::NRES, (j / W::NRES) & 1);   // only the last tile can be partial
-    if (io.ctid < 32) trace_ev(A, j, 15);
     if (staged) {
       // in chunks of CH units: all loads of a chunk first (q_s and sRes could alias as far as the
       // compiler knows), then its stores
@@ -845,6 +986,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       }
     }
     if (io.ctid < 32) trace_ev(A, j, 6);
+    trace_w(A, j, 1);
     if (EPI) continue;   // buffers are released after the next XV_FULL (above)
     if (staged) {
       // every thread that wrote the staged tiles orders its generic-proxy stores before the
@@ -930,6 +1072,10 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   // Producers take the HIGH warp ids: the SMSP arbiter issues highest-wid-first, so their
   // short FP64 chains win the shared FP64/DMMA pipe and the consumers fill the remaining slots.
   const bool is_producer = warp >= W::CW;
+  if constexpr (W::SMR) {
+    if (is_producer) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(W::PREG));
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(W::CREG));
+  }
   if (is_producer) {
     const int ptid = tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
@@ -983,6 +1129,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const int fbase = pwarp * W::NSEG + seg;
       double qp[W::FPASS][5];
       face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
+      if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       if (ptid < 32) trace_ev(A, j, 10);
@@ -1005,40 +1152,15 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           if constexpr (SKIPV) {
             if (rr * PT + (W::PW - 1 - pwarp) * 32 >= EB * NP) continue;
           }
+          if constexpr (W::CTAIL) {
+            if (rr == VR - 1 && j > 0 && ne == EB) continue;   // the consumers computed it
+          }
           const int idx = SKIPV ? (W::PW - 1 - pwarp) * 32 + lane + rr * PT : ptid + rr * PT;
-          const bool inb = idx < EB * NP;
-          const int ic = inb ? idx : 0;
-          const int e = ic / NP, n = ic - e * NP;
-          const bool act = inb && e < ne;
-          const double* q = q_s + e * 5 * NP + n;
-          const double rho = q[0], mx = q[NP], my = q[2 * NP], mz = q[3 * NP], E = q[4 * NP];
-          const double ri = rcp_nr(rho);
-          const double u = mx * ri, v = my * ri, w = mz * ri;
-          const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-          if (act && !state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[e0 + e]);
-          const double* G = g_s + e * GEO;
-          const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
-          double f[3][5];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double cx = G[3 * d], cy = G[3 * d + 1], cz = G[3 * d + 2];
-            const double U = cx * u + cy * v + cz * w;   // contravariant velocity along xi_d
-            f[d][0] = rho * U;
-            f[d][1] = fma(cx, pd, mx * U);
-            f[d][2] = fma(cy, pd, my * U);
-            f[d][3] = fma(cz, pd, mz * U);
-            f[d][4] = Ep * U;
-          }
-          if (inb) {
-            double* xr = sXv + (e * 5) * XSV + n;
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-#pragma unroll
-              for (int c = 0; c < 5; ++c) xr[c * XSV + d * NP] = act ? f[d][c] : 0.0;
-          }
+          vol_node<N, XSV>(A, idx, q_s, g_s, e0, ne, gm1, sXv, EB * NP);
         }
       }
       if (ptid < 32) trace_ev(A, j, 11);
+      trace_w(A, j, 0);
       nbar_arrive(W::BAR_XV_FULL, NT);
       // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1;
       //      the Q_EMPTY sync also covers every producer thread having left tile j-1)
@@ -1057,6 +1179,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ptid < 32) trace_ev(A, j, 13);
       face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
       if (ptid < 32) trace_ev(A, j, 14);
+      trace_w(A, j, 1);
       nbar_arrive(W::BAR_XF_FULL, NT);
     }
   } else {

@@ -17,13 +17,15 @@ s.set_state(configs.initial_state(cfg, s.nodes()))
 dt = s.stable_dt(0.5)
 s.step(dt, 2)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * 1024)()
+buf = (C.c_ulonglong * 4096)()
 f = dg._lib.dg_debug_trace
 f.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_int]
 f.restype = C.c_int
-assert f(s.ctx, buf, 1024) == 0
-t = np.array(buf, dtype=np.int64).reshape(64, 16)
-names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi", 6: "C eloop", 7: "C barC", 15: "C reswait",
+assert f(s.ctx, buf, 4096) == 0
+all_ = np.array(buf, dtype=np.int64)
+t = all_[:1024].reshape(64, 16)
+w = all_[1024:1024 + 48 * 32].reshape(48, 16, 2)
+names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi", 6: "C eloop", 7: "C barC", 15: "P gathered",
          8: "P start", 9: "P tma", 10: "P XVempty", 11: "P vol", 12: "P fetch", 13: "P XFempty", 14: "P face"}
 if cfg.order >= 5:
     names = {0: "start", 1: "inputs", 2: "gathers", 3: "Xfree", 4: "vol", 5: "face", 6: "Xsync", 7: "gemm",
@@ -36,3 +38,8 @@ for j in range(2, 8):
     print(f"tile {j}: " + "  ".join(f"{names[e]}={row[e] - t0}" for e in sorted(names, key=lambda e: row[e])))
 per = (t[10, 0] - t[2, 0]) / 8
 print("cycles per tile (tiles 2..10):", per)
+if cfg.order <= 4:
+    print("per warp (consumers: GEMMs done / epilogue done; producers: volume done / face done), relative to C start:")
+    for j in range(3, 7):
+        base = t[j, 0]
+        print(f"tile {j}: " + "  ".join(f"w{k}:{w[j, k, 0] - base}/{w[j, k, 1] - base}" for k in range(16)))
