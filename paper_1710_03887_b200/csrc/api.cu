@@ -13,6 +13,7 @@
 #include "ctx.h"
 #include "kernels.cuh"
 #include "spectrum.cuh"
+#include "modal.cuh"
 
 namespace {
 
@@ -209,6 +210,7 @@ dgk::StageArgs base_args(dg_ctx* c, double t) {
   A.tbl = c->dtbl;
   A.tblf = c->dtbl + 96 * c->Nfp;
   A.fmask = c->dtbl + 2 * 96 * c->Nfp;
+  A.mtid = c->dmtid;
   A.flag = c->dflag;
   A.gid = c->dgid;
   A.Kpub = int(c->K);
@@ -383,6 +385,7 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   c->dgid = reinterpret_cast<int64_t*>(take(size_t(c->K) * 8));
   c->dop = reinterpret_cast<double*>(take(op_host(c).size() * 8));
   c->dtbl = reinterpret_cast<uint8_t*>(take(2 * 96 * c->Nfp + 4 * c->Nfp));
+  c->dmtid = c->mtid.empty() ? nullptr : reinterpret_cast<uint8_t*>(take(c->mtid.size()));
   const size_t rec = size_t(5) * c->Nfp * 8;
   c->dsend = reinterpret_cast<double*>(take(c->nsend * rec));
   c->drecv = reinterpret_cast<double*>(take(c->nrecv * rec));
@@ -412,6 +415,7 @@ dg_status dg_bind_workspace(dg_ctx* c, void* dptr, size_t nbytes, void* stream) 
   all.insert(all.end(), c->tblf.begin(), c->tblf.end());
   all.insert(all.end(), c->fmask8.begin(), c->fmask8.end());
   CUDA_TRY(c, cudaMemcpyAsync(c->dtbl, all.data(), all.size(), cudaMemcpyHostToDevice, st));
+  if (c->dmtid) CUDA_TRY(c, cudaMemcpyAsync(c->dmtid, c->mtid.data(), c->mtid.size(), cudaMemcpyHostToDevice, st));
   if (c->nsend) {
     CUDA_TRY(c, cudaMemcpyAsync(c->dselem, c->send_elem.data(), c->nsend * 4, cudaMemcpyHostToDevice, st));
     CUDA_TRY(c, cudaMemcpyAsync(c->dsface, c->send_face.data(), c->nsend, cudaMemcpyHostToDevice, st));

@@ -39,6 +39,7 @@ struct dg_ctx {
   std::vector<int32_t> nbr;      // K x 4: neighbour internal index / halo record / -1
   std::vector<uint8_t> code;     // K x 4: f2*6+sigma | 32+f2*6+sigma | 64+tag
   std::vector<uint8_t> tbl, tblf, fmask8;   // neighbour node tables (uint8)
+  std::vector<uint8_t> mtid;     // modal scheme: K x 4 x (own, neighbour) face-point table ids
   std::vector<double> xyz;       // 3 x K x Np node coordinates, PUBLIC element order
   std::vector<double> opfrag;    // B-fragment operator for the DMMA contraction
 
@@ -63,6 +64,7 @@ struct dg_ctx {
   int64_t* dgid = nullptr;
   double* dop = nullptr;
   uint8_t* dtbl = nullptr;     // tbl | tblf | fmask
+  uint8_t* dmtid = nullptr;    // K x 8 (modal scheme)
   double* dsend = nullptr;
   double* drecv = nullptr;
   int32_t* dselem = nullptr;

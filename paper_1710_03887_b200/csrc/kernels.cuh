@@ -51,6 +51,7 @@ struct StageArgs {
   const uint8_t* tbl;     // [4][4][6][Nfp] neighbour volume node  (local neighbours)
   const uint8_t* tblf;    // [4][4][6][Nfp] neighbour face-local node (halo records)
   const uint8_t* fmask;   // [4][Nfp]
+  const uint8_t* mtid;    // [K][4][2] modal face-point table ids (own, neighbour)
   int* flag;              // [0] blow-up flag, [1] element id (global)
   const int64_t* gid;     // [K] global element id (for error messages)
   int e_begin, e_end;     // element range of this launch
@@ -115,13 +116,13 @@ __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   }
 }
 
-// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*2 + k, tiles < 48
+// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*4 + k (k < 4), tiles < 48
 __device__ __forceinline__ void trace_w(const StageArgs& A, int j, int k) {
   if (DG_TRACE && blockIdx.x == 0 && j < 48 && A.trace) {
     __syncwarp();
     unsigned long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 2 + k] = t;
+    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 4 + k] = t;
   }
 }
 
@@ -666,6 +667,9 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0)
 #ifndef DG_SBV
 #define DG_SBV 0
 #endif
+#ifndef DG_STIE
+#define DG_STIE 0
+#endif
 template <int N>
 struct M8Plan {
   static constexpr int MT8 = WS<N>::ROWS / 8;
@@ -693,10 +697,12 @@ struct M8Plan {
       int best = 0;
       for (int w = 1; w < CW; ++w) {
         const int cb = WSI + (ns[best] ? 0 : SBV), cc = WSI + (ns[w] ? 0 : SBV);
-        // with a B-load term, ties go to a warp that already loads the odd tile's B values
+        // with a B-load term, ties go to a warp that already loads the odd tile's B values;
+        // DG_STIE: remaining ties go to the later warp (fewer pairs: the singles' reduction and
+        // epilogue then stay off the warps with the longest contraction)
         const int a = ((smsp[w % 4] + cc) * 4096 + load[w] + cc) * 2 + (SBV > 0 && ns[w] == 0);
         const int b = ((smsp[best % 4] + cb) * 4096 + load[best] + cb) * 2 + (SBV > 0 && ns[best] == 0);
-        if (a < b) best = w;
+        if (a < b || (DG_STIE && a == b)) best = w;
       }
       const int c = WSI + (ns[best] ? 0 : SBV);
       load[best] += c;
@@ -911,7 +917,31 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 4);
     trace_w(A, j, 0);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
-    if (SDF) {   // sum the singles' partial products over the 4 lanes of a row; lane t keeps column t
+#ifndef DG_SRED2
+#define DG_SRED2 1
+#endif
+    if (SDF && DG_SRED2) {
+      // sum the singles' partial products over the 4 lanes of a row, lane t keeping column t, as
+      // a transposing butterfly (3 shuffles per single instead of 2 GS): step 1 (xor 1) each lane
+      // keeps the columns of its parity, step 2 (xor 2) the one of its half; all singles' shuffles
+      // of a step are issued together
+      const bool o1 = t4 & 1, o2 = (t4 & 2) != 0;
+      double k0[NSING > 0 ? NSING : 1], k1[NSING > 0 ? NSING : 1];
+#pragma unroll
+      for (int k = 0; k < NSING; ++k) {
+        const double c0 = sacc[k][0], c1 = W::GS > 1 ? sacc[k][1] : 0.0;
+        const double c2 = W::GS > 2 ? sacc[k][2] : 0.0, c3 = W::GS > 3 ? sacc[k][3] : 0.0;
+        const double s0 = __shfl_xor_sync(0xffffffffu, o1 ? c0 : c1, 1);
+        const double s1 = __shfl_xor_sync(0xffffffffu, o1 ? c2 : c3, 1);
+        k0[k] = (o1 ? c1 : c0) + s0;   // column o1
+        k1[k] = (o1 ? c3 : c2) + s1;   // column 2 + o1
+      }
+#pragma unroll
+      for (int k = 0; k < NSING; ++k) {
+        const double s = __shfl_xor_sync(0xffffffffu, o2 ? k0[k] : k1[k], 2);
+        acc[2 * NPAIR + k][0] = (o2 ? k1[k] : k0[k]) + s;   // column 2 o2 + o1 = t
+      }
+    } else if (SDF) {   // sum the singles' partial products over the 4 lanes of a row; lane t keeps column t
 #pragma unroll
       for (int k = 0; k < NSING; ++k) {
         double mine = 0.0;
@@ -925,12 +955,17 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         acc[2 * NPAIR + k][0] = mine;
       }
     }
+    trace_w(A, j, 2);
     const bool staged = MODE == MODE_UPDATE && ne == EB;
     if (staged) mbar_wait(io.barRes + j % W::NRES, (j / W::NRES) & 1);   // only the last tile can be partial
+    trace_w(A, j, 3);
     if (staged) {
       // in chunks of CH units: all loads of a chunk first (q_s and sRes could alias as far as the
       // compiler knows), then its stores
-      constexpr int CH = 4;
+#ifndef DG_ECH
+#define DG_ECH 4
+#endif
+      constexpr int CH = DG_ECH;
 #pragma unroll
       for (int u0 = 0; u0 < NSLOT; u0 += CH) {
         double rv[CH][2], qv[CH][2];
@@ -1874,19 +1909,23 @@ __global__ void __launch_bounds__(MW<P>::NT, MW<P>::MINB) modal_warp_kernel(cons
       const int k = k0 + ee;
       const double* fv_s = ws + ee * ES + W::E_FV;
       const double* fs_s = ws + ee * ES + W::E_FS;
-      double acc = 0;
+      // four interleaved partial sums: the 3 NQ + 4 NQF long dot product is a latency chain
+      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double* D = T + M::O_DQ + (a * NP + i) * NQ;
         const double* F = fv_s + (a * 5 + c) * NQ;
-        for (int q = 0; q < NQ; ++q) acc = fma(__ldg(D + q), F[q], acc);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc4[(a * NQ + q) & 3] = fma(__ldg(D + q), F[q], acc4[(a * NQ + q) & 3]);
       }
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
         const double* Pt = T + own_s[ee * 4 + f];
         const double* F = fs_s + c * 4 * NQF + f * NQF;
-        for (int q = 0; q < NQF; ++q) acc = fma(-__ldg(Pt + q * NP + i), F[q], acc);
+#pragma unroll
+        for (int q = 0; q < NQF; ++q) acc4[(f * NQF + q) & 3] = fma(-__ldg(Pt + q * NP + i), F[q], acc4[(f * NQF + q) & 3]);
       }
+      const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       rhs[rr] = acc;
       if (MODE == MODE_UPDATE) {
         const size_t gi = size_t(k) * 5 * NP + ci;

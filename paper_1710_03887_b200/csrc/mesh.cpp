@@ -375,6 +375,31 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
         }
   }
 
+  // ---- modal scheme (reading A23): per face the ids of the tables that evaluate the own and
+  // the neighbour polynomial at the face's integration points -- the points of the owner (the
+  // smaller global id): t < 4 the standard points of face t, t = 4 + (f*4 + f2)*6 + perm the
+  // points of face f carried onto face f2 of the neighbour (refelem.h ModalTables.Pmap)
+  if (c->scheme == DG_SCHEME_MODAL) {
+    static const int PERM_INV_H[6] = {0, 1, 2, 4, 3, 5};
+    c->mtid.assign(size_t(c->K) * 8, 0);
+    for (int64_t l = 0; l < c->K; ++l)
+      for (int f = 0; f < 4; ++f) {
+        const int code = c->code[l * 4 + f];
+        int own = f, nbt = f;
+        if (code < 32) {
+          const int nb = c->nbr[l * 4 + f], f2 = code / 6, sg = code - 6 * f2;
+          if (c->gid[l] < c->gid[nb]) {
+            nbt = 4 + (f * 4 + f2) * 6 + sg;
+          } else {
+            own = 4 + (f2 * 4 + f) * 6 + PERM_INV_H[sg];
+            nbt = f2;
+          }
+        }
+        c->mtid[l * 8 + 2 * f] = uint8_t(own);
+        c->mtid[l * 8 + 2 * f + 1] = uint8_t(nbt);
+      }
+  }
+
   // ---- DMMA B-fragment operator: Op = [-Dr -Ds -Dt 0 LIFT] (Np x KPAD), B[k][n] = Op[n][k];
   // the volume block is padded to a multiple of 4 columns (KVP) so the DMMA k-steps of
   // the volume and face halves of X never straddle (kernels.cuh Shape<N>)

@@ -1,0 +1,318 @@
+// Tile kernel of the paper's modal-quadrature scheme (Appendix A,
+// P:396-419; reading A23).  Same arithmetic as modal_warp_kernel (kernels.cuh), laid
+// out for throughput: a persistent CTA (512 threads) walks tiles of EB elements; the next tile's
+// coefficients, geometry and connectivity arrive by TMA while the current one is processed, the
+// neighbours' coefficients by cp.async, and every phase runs over the whole tile with all
+// threads:
+//   V  values of the tile's polynomials at the (p+1)^3 volume points, contravariant fluxes there
+//      (item = element x point);
+//   F  both traces at the owner's (p+1)^2 points of every face (item = element x face x point):
+//      own = T_own c, neighbour = T_nb c_nb with per-face tables (host-chosen ids: the standard
+//      points of the owner or the owner's points carried onto this face), ghosts at boundaries,
+//      wave speeds; after a barrier the face max and the LLF flux weighted by Fscale w;
+//   P  projection onto the basis, dc_i/dt = sum_q,a (w dpsi_i/dxi_a)(q) Ft_a(q)
+//                                         - sum_f,q psi_i(q_f) [Fscale w F*_n](q_f),
+//      as four interleaved partial sums (item = element x field x mode), and the LSERK update
+//      with coalesced global loads and stores ([K][5][Np] order = item order).
+// Tables live in shared memory (for p = 3 the 96 carried-point tables stay in global memory).
+#pragma once
+#include "kernels.cuh"
+
+namespace dgk {
+
+template <int P>
+struct MT {
+  using M = MS<P>;
+  static constexpr int NP = M::NP, NQ = M::NQ, NQF = M::NQF;
+  static constexpr int EB = P == 1 ? 32 : P == 2 ? 16 : 8;
+  static constexpr int NT = 512;
+  static constexpr int ROWS = 5 * EB;
+  static constexpr bool PMAP_SMEM = P <= 2;
+  // table prefix kept in shared memory: WQ, VQ, DQ, WF, PSTD (+ PMAP for p <= 2)
+  static constexpr int TS = PMAP_SMEM ? M::O_V : M::O_PMAP;
+  static constexpr int FVS = 3 * NQ;    // FV row (element, field): columns a NQ + q
+  static constexpr int FSS = 4 * NQF;   // FS row: columns f NQF + q
+  // input buffer (TMA): coefficients, geometry, neighbours, codes, face table ids
+  static constexpr uint32_t BC_ = uint32_t(EB) * 5 * NP * 8;
+  static constexpr uint32_t BG = uint32_t(EB) * GEO * 8;
+  static constexpr uint32_t BN = uint32_t(EB) * 16;
+  static constexpr uint32_t BK = uint32_t(EB) * 4;
+  static constexpr uint32_t BT = uint32_t(EB) * 8;
+  static constexpr uint32_t BIN = BC_ + BG + BN + BK + BT;
+  static_assert(BC_ % 16 == 0 && BG % 16 == 0 && BN % 16 == 0 && BK % 16 == 0 && BT % 16 == 0, "TMA sizes");
+  // shared-memory layout (bytes)
+  static constexpr size_t O_T = 0;
+  static constexpr size_t O_IN = (size_t(TS) * 8 + 127) / 128 * 128;
+  static constexpr size_t O_CN = O_IN + 2 * size_t(BIN);
+  static constexpr size_t O_FV = O_CN + size_t(EB) * 20 * NP * 8;
+  static constexpr size_t O_FS = O_FV + size_t(ROWS) * FVS * 8;
+  static constexpr size_t O_LAM = O_FS + size_t(ROWS) * FSS * 8;
+  static constexpr size_t O_BAR = O_LAM + size_t(EB) * 4 * NQF * 8;
+  static constexpr size_t SMEM = O_BAR + 16;
+  static_assert(SMEM <= 227 * 1024, "modal tile does not fit in shared memory");
+  static constexpr int FR = (EB * 4 * NQF + NT - 1) / NT;   // face rounds
+  static constexpr int PR = (ROWS * NP + NT - 1) / NT;      // projection rounds
+};
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArgs A) {
+  using M = MS<P>;
+  using W = MT<P>;
+  constexpr int NP = W::NP, NQ = W::NQ, NQF = W::NQF, EB = W::EB, NT = W::NT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sT = reinterpret_cast<double*>(smem + W::O_T);
+  unsigned char* in0 = smem + W::O_IN;
+  double* sCN = reinterpret_cast<double*>(smem + W::O_CN);
+  double* sFV = reinterpret_cast<double*>(smem + W::O_FV);
+  double* sFS = reinterpret_cast<double*>(smem + W::O_FS);
+  double* sLAM = reinterpret_cast<double*>(smem + W::O_LAM);
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(smem + W::O_BAR);
+  const int tid = threadIdx.x;
+  const double* T = A.op;
+  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+
+  for (int i = tid; i < W::TS; i += NT) sT[i] = T[i];
+  if (tid == 0) {
+    mbar_init(&sBar[0], 1);
+    mbar_init(&sBar[1], 1);
+  }
+  __syncthreads();
+  auto ftab = [&](int t) -> const double* {   // face table t: 0-3 standard points, 4+ carried points
+    if (W::PMAP_SMEM || t < 4) return sT + M::O_PSTD + t * NQF * NP;
+    return T + M::O_PSTD + t * NQF * NP;
+  };
+  auto bufC = [&](int b) { return reinterpret_cast<double*>(in0 + b * W::BIN); };
+  auto bufG = [&](int b) { return reinterpret_cast<double*>(in0 + b * W::BIN + W::BC_); };
+  auto bufN = [&](int b) { return reinterpret_cast<int*>(in0 + b * W::BIN + W::BC_ + W::BG); };
+  auto bufK = [&](int b) { return in0 + b * W::BIN + W::BC_ + W::BG + W::BN; };
+  auto bufT = [&](int b) { return in0 + b * W::BIN + W::BC_ + W::BG + W::BN + W::BK; };
+
+  const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
+  const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB; };
+  // full tiles by TMA (thread 0); the partial last tile by plain loads of all threads, zero-filled
+  auto fetch = [&](int jj) {
+    const int e0 = tile_e0(jj);
+    const int b = jj & 1;
+    if (A.e_end - e0 >= EB) {
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&sBar[b], W::BIN);
+        tma_load_1d(bufC(b), A.Qin + size_t(e0) * 5 * NP, W::BC_, &sBar[b]);
+        tma_load_1d(bufG(b), A.geo + size_t(e0) * GEO, W::BG, &sBar[b]);
+        tma_load_1d(bufN(b), A.nbr + size_t(e0) * 4, W::BN, &sBar[b]);
+        tma_load_1d(bufK(b), A.code + size_t(e0) * 4, W::BK, &sBar[b]);
+        tma_load_1d(bufT(b), A.tbl + size_t(e0) * 8, W::BT, &sBar[b]);
+      }
+    } else {
+      const int ne = A.e_end - e0;
+      for (int i = tid; i < EB * 5 * NP; i += NT) bufC(b)[i] = i < ne * 5 * NP ? A.Qin[size_t(e0) * 5 * NP + i] : 0.0;
+      for (int i = tid; i < EB * GEO; i += NT) bufG(b)[i] = i < ne * GEO ? A.geo[size_t(e0) * GEO + i] : 0.0;
+      for (int i = tid; i < EB * 4; i += NT) {
+        bufN(b)[i] = i < ne * 4 ? A.nbr[size_t(e0) * 4 + i] : 0;
+        bufK(b)[i] = i < ne * 4 ? A.code[size_t(e0) * 4 + i] : uint8_t(CODE_BC + 2);
+      }
+      for (int i = tid; i < EB * 8; i += NT) bufT(b)[i] = i < ne * 8 ? A.tbl[size_t(e0) * 8 + i] : uint8_t(0);
+    }
+  };
+  if (nmine > 0) fetch(0);
+  __syncthreads();   // a partial tile 0 stored by plain loads
+
+  for (int j = 0; j < nmine; ++j) {
+    const int e0 = tile_e0(j);
+    const int ne = min(EB, A.e_end - e0);
+    const int b = j & 1;
+    // the other buffer (tile j-1) was released by the barrier that ended tile j-1
+    if (j + 1 < nmine) {
+      if (A.e_end - tile_e0(j + 1) >= EB) fetch(j + 1);
+    }
+    if (ne == EB) mbar_wait(&sBar[b], (j >> 1) & 1);
+    const double* cS = bufC(b);
+    const double* gS = bufG(b);
+    const int* nS = bufN(b);
+    const uint8_t* kS = bufK(b);
+    const uint8_t* tS = bufT(b);
+
+    // ---- neighbours' coefficients (cp.async; waited for before the face phase)
+    for (int i = tid; i < EB * 20 * NP; i += NT) {
+      const int e = i / (20 * NP), r1 = i - e * 20 * NP, f = r1 / (5 * NP), r0 = r1 - f * 5 * NP;
+      const int code = kS[e * 4 + f];
+      if (e < ne && code < CODE_GHOST) cp_async8(sCN + i, A.Qin + size_t(nS[e * 4 + f]) * 5 * NP + r0);
+    }
+
+    // ---- V: values and contravariant fluxes at the volume points
+    for (int v = tid; v < EB * NQ; v += NT) {
+      const int e = v / NQ, q = v - e * NQ;
+      const double* c_s = cS + e * 5 * NP;
+      const double* vq = sT + M::O_VQ + q * NP;
+      double u[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) acc = fma(vq[i], c_s[c * NP + i], acc);
+        u[c] = acc;
+      }
+      const bool act = e < ne;
+      if (!act) u[0] = 1.0, u[4] = 2.5;   // padding elements: a harmless state
+      const double ri = 1.0 / u[0];
+      const double vx = u[1] * ri, vy = u[2] * ri, vz = u[3] * ri;
+      const double p = gm1 * (u[4] - 0.5 * (u[1] * vx + u[2] * vy + u[3] * vz));
+      if (act && !state_ok(u[0], p, u[1], u[2], u[3], u[4])) flag_blowup(A.flag, A.gid[e0 + e]);
+      const double pd = p - A.pref, Ep = u[4] + p;
+      const double* G = gS + e * GEO;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double cx = G[3 * a], cy = G[3 * a + 1], cz = G[3 * a + 2];
+        const double U = cx * vx + cy * vy + cz * vz;
+        double* o = sFV + (e * 5) * W::FVS + a * NQ + q;
+        o[0] = u[0] * U;
+        o[W::FVS] = fma(cx, pd, u[1] * U);
+        o[2 * W::FVS] = fma(cy, pd, u[2] * U);
+        o[3 * W::FVS] = fma(cz, pd, u[3] * U);
+        o[4 * W::FVS] = Ep * U;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- F: both traces at the face points, wave speeds
+    double um[W::FR][5], up[W::FR][5];
+#pragma unroll
+    for (int rr = 0; rr < W::FR; ++rr) {
+      const int v = tid + rr * NT;
+      if (v >= EB * 4 * NQF) break;
+      const int e = v / (4 * NQF), fq = v - e * 4 * NQF, f = fq / NQF, q = fq - f * NQF;
+      const int code = kS[e * 4 + f];
+      const double* Gf = gS + e * GEO + 9 + 4 * f;
+      const double* to = ftab(tS[e * 8 + 2 * f]) + q * NP;
+      const double* c_s = cS + e * 5 * NP;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) acc = fma(to[i], c_s[c * NP + i], acc);
+        um[rr][c] = acc;
+      }
+      if (e >= ne) um[rr][0] = 1.0, um[rr][4] = 2.5;
+      if (code < CODE_GHOST && e < ne) {
+        const double* tn = ftab(tS[e * 8 + 2 * f + 1]) + q * NP;
+        const double* cn = sCN + (e * 4 + f) * 5 * NP;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < NP; ++i) acc = fma(tn[i], cn[c * NP + i], acc);
+          up[rr][c] = acc;
+        }
+      } else if (e < ne) {
+        ghost_trace(A, code - CODE_BC, um[rr], Gf[0], Gf[1], Gf[2], up[rr]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) up[rr][c] = um[rr][c];
+      }
+      auto speed = [&](const double (&w)[5]) {
+        const double ri = 1.0 / w[0];
+        const double un = (w[1] * Gf[0] + w[2] * Gf[1] + w[3] * Gf[2]) * ri;
+        const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+        return fabs(un) + sqrt(gamma * p * ri);
+      };
+      sLAM[v] = fmax(speed(um[rr]), speed(up[rr]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < W::FR; ++rr) {
+      const int v = tid + rr * NT;
+      if (v >= EB * 4 * NQF) break;
+      const int e = v / (4 * NQF), fq = v - e * 4 * NQF, f = fq / NQF, q = fq - f * NQF;
+      const double* Gf = gS + e * GEO + 9 + 4 * f;
+      const double nx = Gf[0], ny = Gf[1], nz = Gf[2];
+      double lam = sLAM[v];
+      if (A.lambda_mode == 0) {
+#pragma unroll
+        for (int qq = 0; qq < NQF; ++qq) lam = fmax(lam, sLAM[e * 4 * NQF + f * NQF + qq]);
+      }
+      auto nflux = [&](const double (&w)[5], double* fo) {
+        const double ri = 1.0 / w[0];
+        const double un = (w[1] * nx + w[2] * ny + w[3] * nz) * ri;
+        const double p = gm1 * (w[4] - 0.5 * (w[1] * w[1] + w[2] * w[2] + w[3] * w[3]) * ri);
+        const double pd = p - A.pref;
+        fo[0] = w[0] * un;
+        fo[1] = fma(pd, nx, w[1] * un);
+        fo[2] = fma(pd, ny, w[2] * un);
+        fo[3] = fma(pd, nz, w[3] * un);
+        fo[4] = (w[4] + p) * un;
+      };
+      double fm[5], fp[5];
+      nflux(um[rr], fm);
+      nflux(up[rr], fp);
+      const double sc = e < ne ? Gf[3] * sT[M::O_WF + q] : 0.0;
+      double* fs = sFS + (e * 5) * W::FSS + fq;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) fs[c * W::FSS] = sc * (0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[rr][c] - um[rr][c]));
+    }
+    __syncthreads();
+
+    // ---- P: projection onto the basis and the update (or rhs out)
+    double rhs[W::PR];
+#pragma unroll
+    for (int rr = 0; rr < W::PR; ++rr) {
+      const int v = tid + rr * NT;
+      rhs[rr] = 0.0;
+      if (v >= W::ROWS * NP) break;
+      const int row = v / NP, i = v - row * NP, e = row / 5;
+      const double* fv = sFV + row * W::FVS;
+      const double* fs = sFS + row * W::FSS;
+      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double* D = sT + M::O_DQ + (a * NP + i) * NQ;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc4[(a * NQ + q) & 3] = fma(D[q], fv[a * NQ + q], acc4[(a * NQ + q) & 3]);
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const double* Pt = ftab(tS[e * 8 + 2 * f]) + i;
+#pragma unroll
+        for (int q = 0; q < NQF; ++q)
+          acc4[(f * NQF + q) & 3] = fma(-Pt[q * NP], fs[f * NQF + q], acc4[(f * NQF + q) & 3]);
+      }
+      const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+      rhs[rr] = acc;
+      if (MODE == MODE_UPDATE && e < ne) {
+        const size_t gi = size_t(e0) * 5 * NP + v;
+        const double r2 = fma(A.a, A.res[gi], A.dt * acc);
+        A.res[gi] = r2;
+        A.Qout[gi] = fma(A.b, r2, cS[v]);
+      }
+    }
+    if (MODE == MODE_RHS) {   // V (dc/dt) into the public layout, staged in the FV region
+      __syncthreads();
+#pragma unroll
+      for (int rr = 0; rr < W::PR; ++rr) {
+        const int v = tid + rr * NT;
+        if (v < W::ROWS * NP) sFV[v] = rhs[rr];
+      }
+      __syncthreads();
+      for (int v = tid; v < ne * 5 * NP; v += NT) {
+        const int e = v / (5 * NP), cn = v - e * 5 * NP, c = cn / NP, n = cn - c * NP;
+        const double* r_s = sFV + e * 5 * NP + c * NP;
+        double acc = 0.0;
+        for (int i = 0; i < NP; ++i) acc = fma(__ldg(T + M::O_V + n * NP + i), r_s[i], acc);
+        A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = acc;
+      }
+    }
+    __syncthreads();   // the tile's buffers may be refilled / overwritten by tile j+1 (and j+2)
+    if (j + 1 < nmine && A.e_end - tile_e0(j + 1) < EB) {
+      fetch(j + 1);    // the partial last tile, by plain loads
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace dgk
