@@ -165,8 +165,32 @@ cudaError_t launch_modal_p(const dgk::StageArgs& A, int max_ctas, cudaStream_t s
   return cudaGetLastError();
 }
 
+// the modal tile kernel (modal.cuh): one persistent CTA per SM
+template <int P, int MODE>
+cudaError_t launch_modal_tile_p(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  using W = dgk::MT<P>;
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::modal_tile_kernel<P, MODE>, W::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  const int nel = A.e_end - A.e_begin;
+  if (nel <= 0) return cudaSuccess;
+  dgk::modal_tile_kernel<P, MODE><<<stage_grid((nel + W::EB - 1) / W::EB, max_ctas), W::NT, W::SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
+#ifndef DG_MODAL_TILE
+#define DG_MODAL_TILE 1
+#endif
 template <int MODE>
 cudaError_t launch_modal(int P, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  if (DG_MODAL_TILE) {
+    switch (P) {
+      case 1: return launch_modal_tile_p<1, MODE>(A, max_ctas, st);
+      case 2: return launch_modal_tile_p<2, MODE>(A, max_ctas, st);
+      case 3: return launch_modal_tile_p<3, MODE>(A, max_ctas, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (P) {
     case 1: return launch_modal_p<1, MODE>(A, max_ctas, st);
     case 2: return launch_modal_p<2, MODE>(A, max_ctas, st);
@@ -339,6 +363,7 @@ size_t dg_workspace_bytes(const dg_ctx* c) {
   b += align256(size_t(c->K) * dgk::GEO * 8);                      // geo
   b += align256(size_t(c->K) * 16) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 4) + align256(size_t(c->K) * 8);
   b += align256(op_host(c).size() * 8) + align256(2 * 96 * c->Nfp + 4 * c->Nfp);
+  if (!c->mtid.empty()) b += align256(c->mtid.size());                // modal face-point table ids
   const size_t rec = size_t(5) * c->Nfp * 8;
   b += align256(c->nsend * rec) + align256(c->nrecv * rec) + align256(c->nsend * 4) + align256(c->nsend);
   b += align256(64) + align256(4096 * 8);
@@ -354,7 +379,7 @@ dg_status dg_memory_report(const dg_ctx* c, size_t bytes[7]) {
   bytes[1] = st;
   bytes[2] = st;
   bytes[3] = size_t(c->K) * dgk::GEO * 8;
-  bytes[4] = size_t(c->K) * (16 + 4 + 4 + 8);
+  bytes[4] = size_t(c->K) * (16 + 4 + 4 + 8) + c->mtid.size();
   bytes[5] = op_host(c).size() * 8 + 2 * 96 * c->Nfp + 4 * c->Nfp + size_t(DG_MAX_SENSORS) * (c->Np * 8 + 4);
   bytes[6] = (c->nsend + c->nrecv) * rec + c->nsend * 5;
   return DG_OK;

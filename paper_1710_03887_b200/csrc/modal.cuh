@@ -20,6 +20,13 @@
 
 namespace dgk {
 
+#ifndef DG_MI    // interpolation to the volume points on DMMA (1) or DFMA dot products (0)
+#define DG_MI 1
+#endif
+#ifndef DG_MFP   // face projection: 1 = item (row, face) for every mode, 0 = item (row, mode)
+#define DG_MFP 0
+#endif
+
 template <int P>
 struct MT {
   using M = MS<P>;
@@ -30,7 +37,24 @@ struct MT {
   static constexpr bool PMAP_SMEM = P <= 2;
   // table prefix kept in shared memory: WQ, VQ, DQ, WF, PSTD (+ PMAP for p <= 2)
   static constexpr int TS = PMAP_SMEM ? M::O_V : M::O_PMAP;
-  static constexpr int FVS = 3 * NQ;    // FV row (element, field): columns a NQ + q
+  // volume projection on the FP64 tensor cores (DMMA m8n8k4): rows (element, field), k = a NQ + q
+  // (padded to KVP), n = mode (padded to NPAD); FV rows strided == 4 or 12 (mod 16) doubles so
+  // the A fragments are conflict-free
+  static constexpr int KV = 3 * NQ, KVP = (KV + 3) / 4 * 4, KS = KVP / 4;
+  static constexpr int NPAD = (NP + 7) / 8 * 8, NTL = NPAD / 8;
+  static constexpr int fvs() {
+    int x = KVP;
+    while (x % 16 != 4 && x % 16 != 12) ++x;
+    return x;
+  }
+  static constexpr int FVS = fvs();     // FV row (element, field): columns a NQ + q
+  static constexpr int MT8 = ROWS / 8, UNITS = MT8 * NTL;
+  // interpolation to the volume points on DMMA: A = the tile's coefficients as loaded ([row][NP];
+  // k past NP meets zero B rows -- the values read there are the next row's coefficients or the
+  // geometry behind the block, finite), n = point (NQ padded to NTQ tiles), result into the FS
+  // buffer (free until the face phase) with row stride FSS >= NQ
+  static constexpr int KI = (NP + 3) / 4 * 4, KSI = KI / 4, NTQ = (NQ + 7) / 8, UNITS_I = MT8 * NTQ;
+  static_assert(ROWS % 8 == 0, "DMMA row tiles");
   static constexpr int FSS = 4 * NQF;   // FS row: columns f NQF + q
   // input buffer (TMA): coefficients, geometry, neighbours, codes, face table ids
   static constexpr uint32_t BC_ = uint32_t(EB) * 5 * NP * 8;
@@ -47,7 +71,11 @@ struct MT {
   static constexpr size_t O_FV = O_CN + size_t(EB) * 20 * NP * 8;
   static constexpr size_t O_FS = O_FV + size_t(ROWS) * FVS * 8;
   static constexpr size_t O_LAM = O_FS + size_t(ROWS) * FSS * 8;
-  static constexpr size_t O_BAR = O_LAM + size_t(EB) * 4 * NQF * 8;
+  static constexpr size_t O_FR = O_LAM + size_t(EB) * 4 * NQF * 8;       // B fragments of the volume projection
+  static constexpr size_t O_FI = O_FR + size_t(KS) * NTL * 32 * 8;         // B fragments of the interpolation
+  static constexpr size_t O_RV = O_CN;   // volume-projection result [ROWS][NP] (the neighbours' coefficients are dead by then)
+  static_assert(size_t(ROWS) * NP <= size_t(EB) * 20 * NP && 4 * NQF >= NQ, "buffer aliases");
+  static constexpr size_t O_BAR = O_FI + size_t(KSI) * NTQ * 32 * 8;
   static constexpr size_t SMEM = O_BAR + 16;
   static_assert(SMEM <= 227 * 1024, "modal tile does not fit in shared memory");
   static constexpr int FR = (EB * 4 * NQF + NT - 1) / NT;   // face rounds
@@ -71,12 +99,29 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
   double* sFV = reinterpret_cast<double*>(smem + W::O_FV);
   double* sFS = reinterpret_cast<double*>(smem + W::O_FS);
   double* sLAM = reinterpret_cast<double*>(smem + W::O_LAM);
+  double* sFR = reinterpret_cast<double*>(smem + W::O_FR);
+  double* sRV = reinterpret_cast<double*>(smem + W::O_RV);
   uint64_t* sBar = reinterpret_cast<uint64_t*>(smem + W::O_BAR);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const double* T = A.op;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
 
   for (int i = tid; i < W::TS; i += NT) sT[i] = T[i];
+  // B fragments of (w dpsi_i/dxi_a)(q): lane holds B[k = 4 ks + t][n = 8 nt + g] = DQ(a, n, q), k = a NQ + q
+  for (int idx = tid; idx < W::KS * W::NTL * 32; idx += NT) {
+    const int ks = idx / (W::NTL * 32), r = idx - ks * W::NTL * 32, nt = r >> 5, ln = r & 31;
+    const int k = 4 * ks + (ln & 3), n = nt * 8 + (ln >> 2);
+    const int a = k / NQ, q = k - a * NQ;
+    sFR[idx] = (k < W::KV && n < NP) ? T[M::O_DQ + (a * NP + n) * NQ + q] : 0.0;
+  }
+  for (int i = tid; i < W::ROWS * W::FVS; i += NT) sFV[i] = 0.0;   // padding columns stay 0
+  double* sFI = reinterpret_cast<double*>(smem + W::O_FI);
+  // B fragments of psi_i(q): lane holds B[k = 4 ks + t][n = 8 nt + g] = VQ(q = n, i = k)
+  for (int idx = tid; idx < W::KSI * W::NTQ * 32; idx += NT) {
+    const int ks = idx / (W::NTQ * 32), r = idx - ks * W::NTQ * 32, nt = r >> 5, ln = r & 31;
+    const int k = 4 * ks + (ln & 3), n = nt * 8 + (ln >> 2);
+    sFI[idx] = (k < NP && n < NQ) ? T[M::O_VQ + n * NP + k] : 0.0;
+  }
   if (tid == 0) {
     mbar_init(&sBar[0], 1);
     mbar_init(&sBar[1], 1);
@@ -107,7 +152,7 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
         tma_load_1d(bufG(b), A.geo + size_t(e0) * GEO, W::BG, &sBar[b]);
         tma_load_1d(bufN(b), A.nbr + size_t(e0) * 4, W::BN, &sBar[b]);
         tma_load_1d(bufK(b), A.code + size_t(e0) * 4, W::BK, &sBar[b]);
-        tma_load_1d(bufT(b), A.tbl + size_t(e0) * 8, W::BT, &sBar[b]);
+        tma_load_1d(bufT(b), A.mtid + size_t(e0) * 8, W::BT, &sBar[b]);
       }
     } else {
       const int ne = A.e_end - e0;
@@ -117,7 +162,7 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
         bufN(b)[i] = i < ne * 4 ? A.nbr[size_t(e0) * 4 + i] : 0;
         bufK(b)[i] = i < ne * 4 ? A.code[size_t(e0) * 4 + i] : uint8_t(CODE_BC + 2);
       }
-      for (int i = tid; i < EB * 8; i += NT) bufT(b)[i] = i < ne * 8 ? A.tbl[size_t(e0) * 8 + i] : uint8_t(0);
+      for (int i = tid; i < EB * 8; i += NT) bufT(b)[i] = i < ne * 8 ? A.mtid[size_t(e0) * 8 + i] : uint8_t(0);
     }
   };
   if (nmine > 0) fetch(0);
@@ -145,18 +190,36 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
       if (e < ne && code < CODE_GHOST) cp_async8(sCN + i, A.Qin + size_t(nS[e * 4 + f]) * 5 * NP + r0);
     }
 
-    // ---- V: values and contravariant fluxes at the volume points
+    // ---- V: values at the volume points (DMMA into the FS buffer), then the contravariant fluxes
+    for (int u0 = warp; DG_MI && u0 < W::UNITS_I; u0 += NT / 32) {
+      const int rt = u0 / W::NTQ, nt = u0 - rt * W::NTQ;
+      double acc[2] = {0.0, 0.0};
+      const double* X = cS + (rt * 8 + g) * NP + t4;
+      const double* B = sFI + nt * 32 + lane;
+#pragma unroll
+      for (int ks = 0; ks < W::KSI; ++ks) dmma_8x8x4(acc, X[4 * ks], B[ks * W::NTQ * 32]);
+      const int n0 = nt * 8 + 2 * t4;
+      double* o = sFS + (rt * 8 + g) * W::FSS;
+      if (n0 < NQ) o[n0] = acc[0];
+      if (n0 + 1 < NQ) o[n0 + 1] = acc[1];
+    }
+    __syncthreads();
     for (int v = tid; v < EB * NQ; v += NT) {
       const int e = v / NQ, q = v - e * NQ;
-      const double* c_s = cS + e * 5 * NP;
-      const double* vq = sT + M::O_VQ + q * NP;
       double u[5];
+      if (DG_MI) {
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        double acc = 0.0;
+        for (int c = 0; c < 5; ++c) u[c] = sFS[(e * 5 + c) * W::FSS + q];
+      } else {
+        const double* c_s = cS + e * 5 * NP;
+        const double* vq = sT + M::O_VQ + q * NP;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) acc = fma(vq[i], c_s[c * NP + i], acc);
-        u[c] = acc;
+        for (int c = 0; c < 5; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < NP; ++i) acc = fma(vq[i], c_s[c * NP + i], acc);
+          u[c] = acc;
+        }
       }
       const bool act = e < ne;
       if (!act) u[0] = 1.0, u[4] = 2.5;   // padding elements: a harmless state
@@ -258,31 +321,71 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
     }
     __syncthreads();
 
-    // ---- P: projection onto the basis and the update (or rhs out)
+    // ---- P1: volume projection on DMMA, (row tile, n tile) units over the warps
+    for (int u = warp; u < W::UNITS; u += NT / 32) {
+      const int rt = u / W::NTL, nt = u - rt * W::NTL;
+      double acc[2] = {0.0, 0.0};
+      const double* X = sFV + (rt * 8 + g) * W::FVS + t4;
+      const double* B = sFR + nt * 32 + lane;
+#pragma unroll 7
+      for (int ks = 0; ks < W::KS; ++ks) dmma_8x8x4(acc, X[4 * ks], B[ks * W::NTL * 32]);
+      const int n0 = nt * 8 + 2 * t4;
+      double* o = sRV + (rt * 8 + g) * NP;
+      if (n0 < NP) o[n0] = acc[0];
+      if (n0 + 1 < NP) o[n0 + 1] = acc[1];
+    }
+    __syncthreads();
+    // ---- P2: face projection, item = (row, face) computing every mode (one fs load feeds NP
+    //      FMAs), summed over the 4 faces of the row (consecutive lanes) by two shuffles, added to
+    //      the volume part
+    for (int v0 = 0; DG_MFP && v0 < W::ROWS * 4; v0 += NT) {
+      const int v = v0 + tid;
+      const bool ok = v < W::ROWS * 4;
+      const int row = ok ? v >> 2 : 0, f = v & 3, e = row / 5;
+      const double* fs = sFS + row * W::FSS + f * NQF;
+      const double* Pt = ftab(tS[e * 8 + 2 * f]);
+      double part[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) part[i] = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQF; ++q) {
+        const double w = fs[q];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) part[i] = fma(Pt[q * NP + i], w, part[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        part[i] += __shfl_xor_sync(0xffffffffu, part[i], 1);
+        part[i] += __shfl_xor_sync(0xffffffffu, part[i], 2);
+      }
+      if (ok && f == 0) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) sRV[row * NP + i] -= part[i];
+      }
+    }
+    __syncthreads();
+    // ---- P3: the update (or rhs out)
     double rhs[W::PR];
 #pragma unroll
     for (int rr = 0; rr < W::PR; ++rr) {
       const int v = tid + rr * NT;
       rhs[rr] = 0.0;
       if (v >= W::ROWS * NP) break;
-      const int row = v / NP, i = v - row * NP, e = row / 5;
-      const double* fv = sFV + row * W::FVS;
-      const double* fs = sFS + row * W::FSS;
-      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+      const int e = v / (5 * NP);
+      double acc = sRV[v];
+      if (!DG_MFP) {
+        const int row = v / NP, i = v - row * NP;
+        const double* fs = sFS + row * W::FSS;
+        double acc4[4] = {acc, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double* D = sT + M::O_DQ + (a * NP + i) * NQ;
+        for (int f = 0; f < 4; ++f) {
+          const double* Pt = ftab(tS[e * 8 + 2 * f]) + i;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) acc4[(a * NQ + q) & 3] = fma(D[q], fv[a * NQ + q], acc4[(a * NQ + q) & 3]);
+          for (int q = 0; q < NQF; ++q)
+            acc4[(f * NQF + q) & 3] = fma(-Pt[q * NP], fs[f * NQF + q], acc4[(f * NQF + q) & 3]);
+        }
+        acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       }
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const double* Pt = ftab(tS[e * 8 + 2 * f]) + i;
-#pragma unroll
-        for (int q = 0; q < NQF; ++q)
-          acc4[(f * NQF + q) & 3] = fma(-Pt[q * NP], fs[f * NQF + q], acc4[(f * NQF + q) & 3]);
-      }
-      const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       rhs[rr] = acc;
       if (MODE == MODE_UPDATE && e < ne) {
         const size_t gi = size_t(e0) * 5 * NP + v;
