@@ -23,8 +23,12 @@ namespace dgk {
 #ifndef DG_MI    // interpolation to the volume points on DMMA (1) or DFMA dot products (0)
 #define DG_MI 1
 #endif
-#ifndef DG_MFP   // face projection: 1 = item (row, face) for every mode, 0 = item (row, mode)
-#define DG_MFP 0
+// face projection: 2 = DMMA per (element, mode tile), 1 = item (row, face), 0 = item (row, mode);
+// default 2 at p = 3 (7.9 -> 9.3 GDOF/s), 0 at p <= 2 (p = 2: 12.8 vs 11.8)
+#ifdef DG_MFP
+#define DG_MFP_P(P) DG_MFP
+#else
+#define DG_MFP_P(P) ((P) >= 3 ? 2 : 0)
 #endif
 
 template <int P>
@@ -338,7 +342,31 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
     // ---- P2: face projection, item = (row, face) computing every mode (one fs load feeds NP
     //      FMAs), summed over the 4 faces of the row (consecutive lanes) by two shuffles, added to
     //      the volume part
-    for (int v0 = 0; DG_MFP && v0 < W::ROWS * 4; v0 += NT) {
+    // DG_MFP == 2: unit = (element, mode tile); A = the element's 5 FS rows (rows 5-7 zero),
+    // B[k = f NQF + q][n = i] = psi_i at the face's points (the element's own face tables)
+    for (int u = warp; DG_MFP_P(P) == 2 && u < EB * W::NTL; u += NT / 32) {
+      const int e = u / W::NTL, nt = u - e * W::NTL;
+      const double* fsr = sFS + (e * 5 + (g < 5 ? g : 0)) * W::FSS;
+      const double* tb[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) tb[f] = ftab(tS[e * 8 + 2 * f]);
+      const int n = nt * 8 + g;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < NQF; ++ks) {
+        const int k = 4 * ks + t4, f = k / NQF, q = k - f * NQF;
+        const double a0 = g < 5 ? fsr[k] : 0.0;
+        const double b0 = n < NP ? tb[f][q * NP + n] : 0.0;
+        dmma_8x8x4(acc, a0, b0);
+      }
+      const int n0 = nt * 8 + 2 * t4;
+      if (g < 5) {
+        double* o = sRV + (e * 5 + g) * NP;
+        if (n0 < NP) o[n0] -= acc[0];
+        if (n0 + 1 < NP) o[n0 + 1] -= acc[1];
+      }
+    }
+    for (int v0 = 0; DG_MFP_P(P) == 1 && v0 < W::ROWS * 4; v0 += NT) {
       const int v = v0 + tid;
       const bool ok = v < W::ROWS * 4;
       const int row = ok ? v >> 2 : 0, f = v & 3, e = row / 5;
@@ -373,7 +401,7 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
       if (v >= W::ROWS * NP) break;
       const int e = v / (5 * NP);
       double acc = sRV[v];
-      if (!DG_MFP) {
+      if (DG_MFP_P(P) == 0) {
         const int row = v / NP, i = v - row * NP;
         const double* fs = sFS + row * W::FSS;
         double acc4[4] = {acc, 0.0, 0.0, 0.0};
