@@ -625,6 +625,15 @@ struct WS {
   static constexpr int TAILN = EB * Shape<N>::NP - (VR - 1) * PT;
   static constexpr bool CTAIL = DG_CTAIL && N == 4 && VR >= 2 && TAILN > 0 && TAILN <= 64 && CW >= 2;
   static constexpr int CT0 = (CW - 2) * 32;   // first consumer thread of the tail
+  // DG_PODD (N = 3): the odd trailing n-tile (4 node columns) is contracted by the producers --
+  // on DMMA, one 8-row tile per producer warp, after their face phase -- together with its part
+  // of the epilogue; the consumers keep only the n-tile pairs.  C3 is consumer-bound (the
+  // producers idle at XV_EMPTY), so this moves work to the side that waits.
+#ifndef DG_PODD
+#define DG_PODD 1
+#endif
+  static constexpr bool PODD = DG_PODD && N == 3 && HS && PW >= ROWS / 8;
+  static constexpr int BARC_N = CT + (PODD ? PT : 0);   // threads meeting at BAR_C
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -674,7 +683,7 @@ template <int N>
 struct M8Plan {
   static constexpr int MT8 = WS<N>::ROWS / 8;
   static constexpr int NPG = WS<N>::NPG, HS = WS<N>::HS;
-  static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N>::CW;
+  static constexpr int P = MT8 * NPG, SG = WS<N>::PODD ? 0 : MT8 * HS, CW = WS<N>::CW;
   static constexpr int CPMAX = (P + CW - 1) / CW;
   static constexpr bool SDF1 = WS<N>::GS > 0 && WS<N>::GS <= 4;
 #ifdef DG_SWSI
@@ -1029,7 +1038,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #ifndef DG_EXP_NOFENCE
       fence_proxy_async();
 #endif
-      nbar_sync(W::BAR_C, W::CT);
+      nbar_sync(W::BAR_C, W::BARC_N);
       if (io.ctid < 32) trace_ev(A, j, 7);
       if (io.ctid == IOT) {
         // Q first: once its bulk read is done the input buffer is free; the residual store is
@@ -1216,6 +1225,51 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       if (ptid < 32) trace_ev(A, j, 14);
       trace_w(A, j, 1);
       nbar_arrive(W::BAR_XF_FULL, NT);
+      if constexpr (W::PODD) {
+        // ---- the odd n-tile of tile j: X complete once every producer warp is past its face terms
+        nbar_sync(W::BAR_P, PT);
+        const bool staged = MODE == MODE_UPDATE && ne == EB;
+        if (pwarp < W::ROWS / 8 && !DG_SKIPQ(1)) {
+          const int g = lane >> 2, t4 = lane & 3, row = pwarp * 8 + g;
+          double acc[2] = {0.0, 0.0};
+          const double* bo = sOp + W::NPG * 64 + lane;
+          const bool bl = lane < 4 * W::GS;
+#pragma unroll 5
+          for (int ks = 0; ks < S::KSV; ++ks)
+            dmma_8x8x4(acc, sXv[row * XSV + 4 * ks + t4], bl ? bo[ks * W::OPW] : 0.0);
+#pragma unroll 5
+          for (int ks = S::KSV; ks < S::KS4; ++ks)
+            dmma_8x8x4(acc, sXf[row * XSF + 4 * (ks - S::KSV) + t4], bl ? bo[ks * W::OPW] : 0.0);
+          if (staged) mbar_wait(&sBar[W::NIN + j % W::NRES], (j / W::NRES) & 1);
+          double* qw = bufQ(buf);
+          double* rw = sRes + (j % W::NRES) * (W::BQ / 8);
+          const int e = row / 5, c = row - 5 * e;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int cn = 2 * t4 + q;
+            if (cn >= W::GS) continue;
+            const int n = (S::NTL - 1) * 8 + cn, li = row * NP + n;
+            if (staged) {
+              const double rr = fma(A.a, rw[li], A.dt * acc[q]);
+              rw[li] = rr;
+              qw[li] = fma(A.b, rr, qw[li]);
+            } else if (e < ne) {
+              if (MODE == MODE_UPDATE) {
+                const size_t gi = size_t(e0) * 5 * NP + li;
+                const double rr = fma(A.a, __ldg(A.res + gi), A.dt * acc[q]);
+                A.res[gi] = rr;
+                A.Qout[gi] = fma(A.b, rr, qw[li]);
+              } else {
+                A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = acc[q];
+              }
+            }
+          }
+        }
+        if (staged) {   // the consumers' bulk stores of the tile wait for these columns too
+          fence_proxy_async();
+          nbar_arrive(W::BAR_C, W::BARC_N);
+        }
+      }
     }
   } else {
     // ======================= consumers: DMMA contraction + LSERK epilogue
