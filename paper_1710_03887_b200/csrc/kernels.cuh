@@ -529,6 +529,8 @@ template <int N>
 struct WS {
 #ifdef DG_WS_EB
   static constexpr int EB = DG_WS_EB;
+#elif defined(DG_WS_EB3)
+  static constexpr int EB = N == 3 ? DG_WS_EB3 : (N <= 2) ? 32 : 16;
 #else
   static constexpr int EB = (N <= 2) ? 32 : 16;
 #endif
@@ -629,11 +631,27 @@ struct WS {
   // on DMMA, one 8-row tile per producer warp, after their face phase -- together with its part
   // of the epilogue; the consumers keep only the n-tile pairs.  C3 is consumer-bound (the
   // producers idle at XV_EMPTY), so this moves work to the side that waits.
-#ifndef DG_PODD
-#define DG_PODD 1
+#ifndef DG_PODD   // measured slower: C3 47.9 vs 64.8 GDOF/s (the producers' chain becomes the bound)
+#define DG_PODD 0
 #endif
   static constexpr bool PODD = DG_PODD && N == 3 && HS && PW >= ROWS / 8;
   static constexpr int BARC_N = CT + (PODD ? PT : 0);   // threads meeting at BAR_C
+  // DG_CHI: consumers take the HIGH warp ids (the SMSP arbiter favours them), producers the low
+  // ones; the SMSP of consumer warp cw stays cw % 4 (PW % 4 == 0)
+#ifndef DG_CHI
+#define DG_CHI 0
+#endif
+  static constexpr bool CHI = DG_CHI && PW % 4 == 0;
+  // DG_PEPI (N = 3, deep buffering): the epilogue is split -- the consumers form res = a res +
+  // dt rhs in place (their only shared-memory pass) and arrive on BAR_E; the producers, who wait
+  // at this point anyway on C3, form Q += b res over the whole tile with conflict-free
+  // contiguous accesses, issue both bulk stores and all residual loads, and reuse the buffers
+  // in program order (no BAR_C, no Q_EMPTY) -- the consumers go straight to the next tile
+#ifndef DG_PEPI   // measured slower: C3 62.2 vs 64.8 GDOF/s
+#define DG_PEPI 0
+#endif
+  static constexpr bool PEPI = DG_PEPI && N == 3 && DEEP && !PODD;
+  static constexpr int BAR_E = 11;
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -814,7 +832,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #define DG_EPI 0
 #endif
   constexpr bool EPI = DG_EPI && MODE == MODE_UPDATE;
-  if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
+  if (MODE == MODE_UPDATE && !W::PEPI && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     const int e0 = A.e_begin + tile * EB;
@@ -985,7 +1003,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             const int n = unit_n(u, q);
             const int li = (unit_mt(u) * 8 + g) * NP + (n < NP ? n : 0);
             rv[u - u0][q] = sRes[li];
-            qv[u - u0][q] = q_s[li];
+            if (!W::PEPI) qv[u - u0][q] = q_s[li];
           }
 #pragma unroll
         for (int u = u0; u < u0 + CH && u < NSLOT; ++u)
@@ -995,6 +1013,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             if (n >= NP) continue;
             const int li = (unit_mt(u) * 8 + g) * NP + n;   // == (e*5 + c)*NP + n
             const double rr = fma(A.a, rv[u - u0][q], A.dt * acc[u][q]);
+            if (W::PEPI) {
+              sRes[li] = rr;
+              continue;
+            }
             const double qn = fma(A.b, rr, qv[u - u0][q]);
             if (EPI) {
               const size_t gi = size_t(e0) * 5 * NP + li;
@@ -1032,6 +1054,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 6);
     trace_w(A, j, 1);
     if (EPI) continue;   // buffers are released after the next XV_FULL (above)
+    if constexpr (W::PEPI) {
+      if (staged) nbar_arrive(W::BAR_E, W::CT + W::PT);   // the producers finish the tile
+      continue;
+    }
     if (staged) {
       // every thread that wrote the staged tiles orders its generic-proxy stores before the
       // async-proxy (TMA) reads of the bulk stores issued after the barrier
@@ -1115,13 +1141,13 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 
   // Producers take the HIGH warp ids: the SMSP arbiter issues highest-wid-first, so their
   // short FP64 chains win the shared FP64/DMMA pipe and the consumers fill the remaining slots.
-  const bool is_producer = warp >= W::CW;
+  const bool is_producer = W::CHI ? warp < W::PW : warp >= W::CW;
   if constexpr (W::SMR) {
     if (is_producer) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(W::PREG));
     else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(W::CREG));
   }
   if (is_producer) {
-    const int ptid = tid - W::CT, pwarp = ptid >> 5;
+    const int ptid = W::CHI ? tid : tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
     const double gm1 = A.gamma - 1.0;
     auto fetch = [&](int jj) {
@@ -1152,6 +1178,38 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         nbar_sync(W::BAR_P, PT);
       }
     };
+    // PEPI: the second half of tile jm's epilogue and its bulk stores (called once the consumers
+    // are through with the tile); the stores of tile jm - 1 are waited for first, which frees
+    // residual buffer (jm - 1) % 2 for tile jm + 1 and input buffer (jm - 1) % 3 for tile jm + 2
+    auto staged_t = [&](int jj) {
+      return MODE == MODE_UPDATE && A.e_end - (A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB) >= EB;
+    };
+    auto res_load = [&](int jj) {   // one thread
+      const int e0r = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&sBar[W::NIN + jj % W::NRES], W::BQ);
+      tma_load_1d(sRes + (jj % W::NRES) * (W::BQ / 8), A.res + size_t(e0r) * 5 * NP, W::BQ, &sBar[W::NIN + jj % W::NRES]);
+    };
+    auto pepi = [&](int jm) {
+      nbar_sync(W::BAR_E, W::CT + W::PT);
+      double* qw = bufQ(jm % W::NIN);
+      const double* rw = sRes + (jm % W::NRES) * (W::BQ / 8);
+      for (int li = ptid; li < EB * 5 * NP; li += PT) qw[li] = fma(A.b, rw[li], qw[li]);
+      fence_proxy_async();
+      nbar_sync(W::BAR_P, PT);
+      if (ptid == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        if (jm + 1 < nmine && staged_t(jm + 1)) res_load(jm + 1);
+        const int e0m = A.e_begin + (int(blockIdx.x) + jm * int(gridDim.x)) * EB;
+        fence_proxy_async();
+        tma_store_1d(A.Qout + size_t(e0m) * 5 * NP, qw, W::BQ);
+        tma_store_1d(A.res + size_t(e0m) * 5 * NP, rw, W::BQ);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    };
+    if constexpr (W::PEPI) {
+      if (ptid == 0 && nmine > 0 && staged_t(0)) res_load(0);
+    }
     if (nmine > 0) fetch(0);
     if (W::NIN == 2 && nmine > 1) fetch(1);   // later full tiles are fetched by the consumers
     for (int j = 0; j < nmine; ++j) {
@@ -1214,12 +1272,25 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           fetch(j + 1);
         }
       } else if (j + 1 < nmine) {
-        if (j + 1 >= W::NIN) nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
+        if (j + 1 >= W::NIN) {
+          if constexpr (W::PEPI) {
+            // the buffer's last user, tile j-2, left by bulk stores issued by thread 0 (pepi):
+            // thread 0 waits for their reads; the partial-tile path of fetch writes with every
+            // producer thread, so they meet thread 0 first
+            if (ptid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            if (A.e_end - (A.e_begin + (int(blockIdx.x) + (j + 1) * int(gridDim.x)) * EB) < EB) nbar_sync(W::BAR_P, PT);
+          } else {
+            nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
+          }
+        }
         fetch(j + 1);
       }
       // ---- face fluxes -> Xf
       if (ptid < 32) trace_ev(A, j, 12);
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
+      if constexpr (W::PEPI) {
+        if (j >= 1 && staged_t(j - 1)) pepi(j - 1);
+      }
       if (ptid < 32) trace_ev(A, j, 13);
       face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
       if (ptid < 32) trace_ev(A, j, 14);
@@ -1271,13 +1342,17 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         }
       }
     }
+    if constexpr (W::PEPI) {
+      if (nmine > 0 && staged_t(nmine - 1)) pepi(nmine - 1);
+      if (ptid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete before exit
+    }
   } else {
     // ======================= consumers: DMMA contraction + LSERK epilogue
     // every warp runs a compile-time-shaped loop over its units so its DMMA chains interleave
     // without run-time branches
     using PL = M8Plan<N>;
-    const int cw = warp;
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, tid, lane};
+    const int cw = W::CHI ? warp - W::PW : warp;
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, W::CHI ? tid - W::PT : tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;

@@ -198,3 +198,26 @@ def test_modal_scheme_limits():
     assert e.value.status == dg.DG_EUNSUPPORTED
     with pytest.raises(dg.DGError):
         dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc, scheme=7)
+
+
+def test_nccl_cta_reservation_arguments():
+    """dg_set_nccl_ctas (SURVEY §8(e) overlap): [0, 64] accepted before dg_comm_init, else DG_EARG."""
+    m = smesh.kuhn_box((2, 2, 2), (0, 0, 0), (1, 1, 1), periodic=(True, True, True))
+    ctx = dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc)
+    try:
+        for n in (0, 2, 64):
+            dg.dg_set_nccl_ctas(ctx, n)
+        for n in (-1, 65):
+            with pytest.raises(dg.DGError) as e:
+                dg.dg_set_nccl_ctas(ctx, n)
+            assert e.value.status == dg.DG_EARG
+    finally:
+        dg.dg_destroy(ctx)
+
+
+def test_spectrum_argument_errors():
+    """dg_spectrum validates its arguments on the host (no launch): NULL pointers, n < 2, m < 1."""
+    for args in ((0, 16, 1, 8, 8), (8, 1, 1, 8, 8), (8, 16, 0, 8, 8), (8, 16, 1, 0, 8), (8, 16, 70000, 8, 8)):
+        with pytest.raises(dg.DGError) as e:
+            dg.dg_spectrum(args[0], args[1], args[2], args[3], args[4], 0)
+        assert e.value.status == dg.DG_EARG
