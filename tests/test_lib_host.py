@@ -203,7 +203,7 @@ def test_modal_scheme_limits():
 def test_nccl_cta_reservation_arguments():
     """dg_set_nccl_ctas (SURVEY §8(e) overlap): [0, 64] accepted before dg_comm_init, else DG_EARG."""
     m = smesh.kuhn_box((3, 3, 3), (0, 0, 0), (1, 1, 1), periodic=(True, True, True))
-    ctx = dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc)
+    ctx = dg.dg_mesh_create(2, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof)
     try:
         for n in (0, 2, 64):
             dg.dg_set_nccl_ctas(ctx, n)
