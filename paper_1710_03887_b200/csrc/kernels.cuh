@@ -1387,7 +1387,9 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 template <int N>
 struct HO {
   using S = Shape<N>;
-  static constexpr int EB = 8, NW = 15, CT = 32 * NW, NT = CT + 32;   // + one loader warp
+  // EB 16 at N <= 4 serves only the DG_HO34 experiment (the phased kernel at N = 3, 4 measured
+  // 38 GDOF/s on C3 and C4 against 64.8 / 55.9 for the warp-specialised kernel)
+  static constexpr int EB = N <= 4 ? 16 : 8, NW = 15, CT = 32 * NW, NT = CT + 32;   // + one loader warp
   static constexpr int ROWS = 5 * EB, MT8 = ROWS / 8;
   static constexpr int XS = S::XS;
   static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
