@@ -661,7 +661,7 @@ constexpr int kunroll() {
 #ifdef DG_KUNROLL
   return DG_KUNROLL;
 #else
-  return N == 4 ? 7 : 6;
+  return N == 4 ? 7 : N == 3 ? 15 : 6;   // N = 3: both loops (15 and 10 k-steps) fully unrolled (C3 64.8 -> 65.7)
 #endif
 }
 
