@@ -531,6 +531,8 @@ struct WS {
   static constexpr int EB = DG_WS_EB;
 #elif defined(DG_WS_EB3)
   static constexpr int EB = N == 3 ? DG_WS_EB3 : (N <= 2) ? 32 : 16;
+#elif defined(DG_WS_EB4)
+  static constexpr int EB = N == 4 ? DG_WS_EB4 : (N <= 2) ? 32 : 16;
 #else
   static constexpr int EB = (N <= 2) ? 32 : 16;
 #endif
@@ -1233,7 +1235,10 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const bool lane_ok = i < NFP && seg < W::NSEG;
       const int fbase = pwarp * W::NSEG + seg;
       double qp[W::FPASS][5];
-      face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
+#ifndef DG_GLATE   // experiment: issue the gathers after the volume phase
+#define DG_GLATE 0
+#endif
+      if (!DG_GLATE) face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
@@ -1289,6 +1294,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         fetch(j + 1);
       }
       // ---- face fluxes -> Xf
+      if (DG_GLATE) face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 12);
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
       if constexpr (W::PEPI) {
