@@ -268,15 +268,16 @@ __device__ __forceinline__ void tma_store_commit_and_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
-template <int XSTR_, int K0_, int K1_>
-struct KBlk {
-  static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_;
+template <int XSTR_, int K0_, int K1_, int XK0_ = K0_>
+struct KBlk {   // k-steps [K0, K1) of a block of X whose first column is k-step XK0
+  static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_, XK0 = XK0_;
 };
 
 // Neighbour traces of NPASS face passes (face of pass u: fbase + u fstride; one face per
 // SEGW-lane segment, lane i < NFP its node i): local neighbour / halo record gathers, or the
 // boundary ghost from the own trace; idle lanes keep a finite filler.
-template <int N, int NPASS>
+// FMB = 0: face = 4 e + f (element-major); FMB = EB: face = f EB + e (face-major, DG_FSPLIT)
+template <int N, int NPASS, int FMB = 0>
 __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                             bool lane_ok, const double* q_s, const double* g_s, const int* n_s,
                                             const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
@@ -294,7 +295,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 #pragma unroll
     for (int u = 0; u < NPASS; ++u) {
       const int face = fbase + u * fstride;
-      const int e = face >> 2, f = face & 3;
+      const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
       ok[u] = !DG_SKIPQ(2) && lane_ok && face < flim && e < ne;
       const int ec = ok[u] ? e : 0;
       code[u] = ok[u] ? int(c_s[ec * 4 + f]) : CODE_BC;
@@ -321,7 +322,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
         for (int c = 0; c < 5; ++c) qp[u][c] = __ldg(q2 + c * NFP);
       } else if (ok[u]) {   // boundary ghost from the own trace (Q of this tile is in shared memory)
         const int face = fbase + u * fstride;
-        const int e = face >> 2, f = face & 3;
+        const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
         const double* G = g_s + e * GEO + 9 + 4 * f;
         const double* q = q_s + e * 5 * NP + node[u];
         double qm[5];
@@ -335,7 +336,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
-    const int e = face >> 2, f = face & 3;
+    const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
 #pragma unroll
     for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
     if (!DG_SKIPQ(2) && lane_ok && face < flim && e < ne) {
@@ -361,7 +362,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 //   Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-)),
 // where the ambient-pressure shift (A14) cancels in n.F(q-) - n.F(q+).  Slots of elements past
 // ne store zeros.
-template <int N, int NPASS, int SEGW, int XSF>
+template <int N, int NPASS, int SEGW, int XSF, int FMB = 0>
 __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                            bool lane_ok, const double* q_s, const double* g_s, const uint8_t* sFm,
                                            const double (&qp)[NPASS][5], double* sXf) {
@@ -381,9 +382,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
-    const bool act = lane_ok && face < flim && (face >> 2) < ne;
+    const bool act = lane_ok && face < flim && (FMB ? face % FMB : face >> 2) < ne;
     const int fc = act ? face : 0;
-    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+    const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
     const double* G = g_s + e * GEO + 9 + 4 * f;
     const double nx = G[0], ny = G[1], nz = G[2];
     const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
@@ -445,9 +446,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
     for (int u = 0; u < NPASS; ++u) {
       const int face = fbase + u * fstride;
       const bool slot = lane_ok && face < flim;
-      const bool act = slot && (face >> 2) < ne;
+      const bool act = slot && (FMB ? face % FMB : face >> 2) < ne;
       const int fc = slot ? face : 0;
-      const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+      const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
       const double hfs = act ? 0.5 * g_s[e * GEO + 9 + 4 * f + 3] : 0.0;
       double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
       if (slot) {
@@ -460,9 +461,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
     const bool slot = lane_ok && face < flim;
-    const bool act = slot && (face >> 2) < ne;
+    const bool act = slot && (FMB ? face % FMB : face >> 2) < ne;
     const int fc = slot ? face : 0;
-    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
+    const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
     const double* G = g_s + e * GEO + 9 + 4 * f;
     const double nx = G[0], ny = G[1], nz = G[2], hfs = act ? 0.5 * G[3] : 0.0;
     const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
@@ -654,6 +655,16 @@ struct WS {
 #endif
   static constexpr bool PEPI = DG_PEPI && N == 3 && DEEP && !PODD;
   static constexpr int BAR_E = 11;
+  // DG_FSPLIT (N = 4): faces in face-major order (pass u = face u of every element); the face
+  // block's first k-steps (faces 0 and 1: 2 Nfp columns) are released after the first two
+  // passes (BAR_XF_FULL), the rest after the last two (BAR_XF_FULL_B), so the consumers' face
+  // contraction starts half a face phase earlier
+#ifndef DG_FSPLIT   // measured slower: C4 53.5 vs 56.1 GDOF/s (two face passes per half lose ILP)
+#define DG_FSPLIT 0
+#endif
+  static constexpr bool FSPLIT = DG_FSPLIT && N == 4 && !FDENSE && NSEG * PW == EB && FPASS == 4;
+  static constexpr int BAR_XF_FULL_B = 12;
+  static constexpr int KSPLIT = Shape<N>::KSV + (2 * Shape<N>::NFP) / 4;   // last k-step needing faces 0, 1 only (+1)
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -864,7 +875,8 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       return unit_nt(u) * 8 + 2 * t4 + q;
     };
     auto kloop = [&](auto xblk) {
-      constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
+      constexpr int XSTR = decltype(xblk)::XSTR, K1 = decltype(xblk)::K1, XK0 = decltype(xblk)::XK0;
+      constexpr int K0 = decltype(xblk)::K0;
       if DG_SKIPQ(1) return;
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
       constexpr int KU = kunroll<N>();
@@ -873,7 +885,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         const double* ob = io.sOp + ks * W::OPW;
 #pragma unroll
         for (int k = 0; k < NPAIR; ++k) {
-          const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+          const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
           const double2 b = *reinterpret_cast<const double2*>(ob + (ntp[k] >> 1) * 64 + 2 * lane);
           dmma_8x8x4(acc[2 * k], a0, b.x);
           dmma_8x8x4(acc[2 * k + 1], a0, b.y);
@@ -884,7 +896,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
-            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
 #pragma unroll
             for (int c = 0; c < W::GS; ++c) sacc[k][c] = fma(a0, bv[c], sacc[k][c]);
           }
@@ -892,7 +904,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           const double bs = lane < 4 * W::GS ? ob[W::NPG * 64 + lane] : 0.0;
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
-            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
+            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
             dmma_8x8x4(acc[2 * NPAIR + k], a0, bs);
           }
         }
@@ -942,7 +954,13 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 
     nbar_sync(W::BAR_XF_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 3);
-    kloop(KBlk<XSF, S::KSV, S::KS4>{});
+    if constexpr (W::FSPLIT) {
+      kloop(KBlk<XSF, S::KSV, W::KSPLIT, S::KSV>{});
+      nbar_sync(W::BAR_XF_FULL_B, NT);
+      kloop(KBlk<XSF, W::KSPLIT, S::KS4, S::KSV>{});
+    } else {
+      kloop(KBlk<XSF, S::KSV, S::KS4>{});
+    }
     if (io.ctid < 32) trace_ev(A, j, 4);
     trace_w(A, j, 0);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
@@ -1238,7 +1256,8 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 #ifndef DG_GLATE   // experiment: issue the gathers after the volume phase
 #define DG_GLATE 0
 #endif
-      if (!DG_GLATE) face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
+      constexpr int FMB = W::FSPLIT ? EB : 0;
+      if (!DG_GLATE) face_gather<N, W::FPASS, FMB>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
@@ -1301,10 +1320,22 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         if (j >= 1 && staged_t(j - 1)) pepi(j - 1);
       }
       if (ptid < 32) trace_ev(A, j, 13);
-      face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
-      if (ptid < 32) trace_ev(A, j, 14);
-      trace_w(A, j, 1);
-      nbar_arrive(W::BAR_XF_FULL, NT);
+      if constexpr (W::FSPLIT) {
+        using QP2 = const double(&)[2][5];
+        face_terms<N, 2, W::SEGW, XSF, FMB>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm,
+                                            reinterpret_cast<QP2>(qp[0]), sXf);
+        nbar_arrive(W::BAR_XF_FULL, NT);
+        face_terms<N, 2, W::SEGW, XSF, FMB>(A, fbase + 2 * W::PW * W::NSEG, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s,
+                                            g_s, sFm, reinterpret_cast<QP2>(qp[2]), sXf);
+        if (ptid < 32) trace_ev(A, j, 14);
+        trace_w(A, j, 1);
+        nbar_arrive(W::BAR_XF_FULL_B, NT);
+      } else {
+        face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
+        if (ptid < 32) trace_ev(A, j, 14);
+        trace_w(A, j, 1);
+        nbar_arrive(W::BAR_XF_FULL, NT);
+      }
       if constexpr (W::PODD) {
         // ---- the odd n-tile of tile j: X complete once every producer warp is past its face terms
         nbar_sync(W::BAR_P, PT);

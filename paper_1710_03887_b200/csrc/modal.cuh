@@ -89,6 +89,9 @@ struct MT {
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int P, int MODE>
@@ -187,11 +190,13 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
     const uint8_t* kS = bufK(b);
     const uint8_t* tS = bufT(b);
 
-    // ---- neighbours' coefficients (cp.async; waited for before the face phase)
-    for (int i = tid; i < EB * 20 * NP; i += NT) {
+    // ---- neighbours' coefficients (16-byte cp.async -- a face's block is 5 Np doubles, a multiple
+    //      of 2 -- waited for before the face phase)
+    for (int i2 = tid; i2 < EB * 10 * NP; i2 += NT) {
+      const int i = 2 * i2;
       const int e = i / (20 * NP), r1 = i - e * 20 * NP, f = r1 / (5 * NP), r0 = r1 - f * 5 * NP;
       const int code = kS[e * 4 + f];
-      if (e < ne && code < CODE_GHOST) cp_async8(sCN + i, A.Qin + size_t(nS[e * 4 + f]) * 5 * NP + r0);
+      if (e < ne && code < CODE_GHOST) cp_async16(sCN + i, A.Qin + size_t(nS[e * 4 + f]) * 5 * NP + r0);
     }
 
     // ---- V: values at the volume points (DMMA into the FS buffer), then the contravariant fluxes
