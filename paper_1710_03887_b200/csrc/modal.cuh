@@ -53,6 +53,15 @@ struct MT {
   }
   static constexpr int FVS = fvs();     // FV row (element, field): columns a NQ + q
   static constexpr int MT8 = ROWS / 8, UNITS = MT8 * NTL;
+  // the k range of each unit is split KP ways so every warp gets work; the KP partial results go
+  // to separate buffers (in the neighbours' coefficient region, dead by then) and are summed in a
+  // fixed order -- deterministic
+  // (DG_MKP=1: measured slower, p = 1 / 2 / 3: 16.9 / 12.3 / 9.5 vs 19.2 / 13.5 / 9.7 GDOF/s)
+#ifdef DG_MKP
+  static constexpr int KP = (64 + UNITS - 1) / UNITS < 4 ? (64 + UNITS - 1) / UNITS : 4;
+#else
+  static constexpr int KP = 1;
+#endif
   // interpolation to the volume points on DMMA: A = the tile's coefficients as loaded ([row][NP];
   // k past NP meets zero B rows -- the values read there are the next row's coefficients or the
   // geometry behind the block, finite), n = point (NQ padded to NTQ tiles), result into the FS
@@ -78,7 +87,7 @@ struct MT {
   static constexpr size_t O_FR = O_LAM + size_t(EB) * 4 * NQF * 8;       // B fragments of the volume projection
   static constexpr size_t O_FI = O_FR + size_t(KS) * NTL * 32 * 8;         // B fragments of the interpolation
   static constexpr size_t O_RV = O_CN;   // volume-projection result [ROWS][NP] (the neighbours' coefficients are dead by then)
-  static_assert(size_t(ROWS) * NP <= size_t(EB) * 20 * NP && 4 * NQF >= NQ, "buffer aliases");
+  static_assert(size_t(KP) * ROWS * NP <= size_t(EB) * 20 * NP && 4 * NQF >= NQ, "buffer aliases");
   static constexpr size_t O_BAR = O_FI + size_t(KSI) * NTQ * 32 * 8;
   static constexpr size_t SMEM = O_BAR + 16;
   static_assert(SMEM <= 227 * 1024, "modal tile does not fit in shared memory");
@@ -331,15 +340,16 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
     __syncthreads();
 
     // ---- P1: volume projection on DMMA, (row tile, n tile) units over the warps
-    for (int u = warp; u < W::UNITS; u += NT / 32) {
-      const int rt = u / W::NTL, nt = u - rt * W::NTL;
+    for (int u = warp; u < W::UNITS * W::KP; u += NT / 32) {
+      const int kp = u % W::KP, u1 = u / W::KP, rt = u1 / W::NTL, nt = u1 - rt * W::NTL;
+      const int ks0 = kp * W::KS / W::KP, ks1 = (kp + 1) * W::KS / W::KP;
       double acc[2] = {0.0, 0.0};
       const double* X = sFV + (rt * 8 + g) * W::FVS + t4;
       const double* B = sFR + nt * 32 + lane;
-#pragma unroll 7
-      for (int ks = 0; ks < W::KS; ++ks) dmma_8x8x4(acc, X[4 * ks], B[ks * W::NTL * 32]);
+#pragma unroll 4
+      for (int ks = ks0; ks < ks1; ++ks) dmma_8x8x4(acc, X[4 * ks], B[ks * W::NTL * 32]);
       const int n0 = nt * 8 + 2 * t4;
-      double* o = sRV + (rt * 8 + g) * NP;
+      double* o = sRV + size_t(kp) * W::ROWS * NP + (rt * 8 + g) * NP;
       if (n0 < NP) o[n0] = acc[0];
       if (n0 + 1 < NP) o[n0 + 1] = acc[1];
     }
@@ -406,6 +416,8 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
       if (v >= W::ROWS * NP) break;
       const int e = v / (5 * NP);
       double acc = sRV[v];
+#pragma unroll
+      for (int kp = 1; kp < W::KP; ++kp) acc += sRV[kp * W::ROWS * NP + v];
       if (DG_MFP_P(P) == 0) {
         const int row = v / NP, i = v - row * NP;
         const double* fs = sFS + row * W::FSS;
