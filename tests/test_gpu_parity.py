@@ -356,14 +356,17 @@ def ws_view(sv, ptr, nbytes):
     return sv.ws[off:off + nbytes]
 
 
+@pytest.mark.parametrize("name,scale", [("C4", 0.12), ("C2", 0.5), ("C1", 1.0)])
 @pytest.mark.parametrize("nparts,split,cap", [(2, False, 0), (3, False, 0), (2, True, 0), (3, True, 2)])
-def test_partition_invariance_emulated(nparts, split, cap):
+def test_partition_invariance_emulated(nparts, split, cap, name, scale):
     """P ranks emulated as P contexts on one GPU, halo records exchanged by device copies
     between the stage-level calls: final state bitwise equal to P = 1.  split: the
     production order of dg_rk_step -- pack, interior launch (which = 1) BEFORE the halo
     arrives, then the boundary launch (which = 2, the range starting at K_int) -- and the
-    same for dg_rhs_compute; cap: every CTA walks several tiles of each range."""
-    cfg = configs.make("C4", scale=0.12)
+    same for dg_rhs_compute; cap: every CTA walks several tiles of each range.  N = 4 (C4),
+    N = 3 (C2: dense face segments, level-by-level gathers from the halo records) and N = 2 on
+    a periodic mesh (C1: the slabs wrap around)."""
+    cfg = configs.make(name, scale=scale)
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
     dt = parity.oracle_dt(o, Q, 0.5)
