@@ -124,3 +124,27 @@ def test_modal_inflow_through_the_stepper(rk, p):
     err = parity.e_state(s.get_state(), o.to_nodal(c), parity.scales(cfg))
     assert err <= parity.STATE_TOL, err
     s.close()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_modal_on_the_horn_mesh_multi_tile(p):
+    """The benchmark geometry (C4: carved horn with wall faces, pass-through box) at 0.1 scale,
+    the grid capped so every CTA walks many tiles of the modal tile kernel (TMA prefetch of the
+    next tile, cp.async neighbour gathers, carried-point face tables on the horn's oblique faces):
+    one RHS and 5 LSERK4 steps against the oracle."""
+    cfg = configs.make("C4", scale=0.1)
+    cfg.order = p
+    o = modal.ModalOracle(parity.oracle_mesh(cfg))
+    Q = _state(o, cfg)
+    s = _solver(cfg)
+    s.set_max_ctas(4)
+    s.set_state(Q)
+    want = o.to_nodal(o.rhs(o.to_modal(Q), 0.0))
+    err = parity.e_rhs(s.rhs(0.0), want, parity.scales(cfg))
+    assert err <= parity.RHS_TOL, err
+    dt = 0.5 * parity.oracle_dt(o.m, Q, 0.5)
+    s.step(dt, 5)
+    c, _, _ = timestep.integrate(lambda cc, tt: o.rhs(cc, tt), o.to_modal(Q), 0.0, dt, 5)
+    err = parity.e_state(s.get_state(), o.to_nodal(c), parity.scales(cfg))
+    assert err <= parity.STATE_TOL, err
+    s.close()
