@@ -1690,9 +1690,13 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       }
     }
     if (warp == 0) trace_ev(A, j, 4);
-    // ---- face terms -> X[:, KVP:KVP+4Nfp)
+    // ---- face terms -> X[:, KVP:KVP+4Nfp)  (DG_HO_F1: the own trace read once, as at N <= 4)
+#ifndef DG_HO_F1   // measured slower at N = 6: C5 23.7 vs 28.4 GDOF/s (32 B of spills)
+#define DG_HO_F1 0
+#endif
     if (!DG_SKIPQ(2)) {
       double rip[H::FPASS], unp[H::FPASS], pp[H::FPASS], lam[H::FPASS], unmv[H::FPASS], pmv[H::FPASS];
+      double dqv[DG_HO_F1 ? H::FPASS : 1][5], gfv[DG_HO_F1 ? H::FPASS : 1][5];
 #pragma unroll
       for (int u = 0; u < H::FPASS; ++u) {
         const int face = warp * H::NSEG + u * H::STRIDE + seg;
@@ -1713,6 +1717,20 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
         const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
         lam[u] = act ? l : 0.0;
+        if (DG_HO_F1) {
+          // n.F(q-) - n.F(q+): the ambient-pressure shift cancels (A14)
+          const double dp = pm - pp[u];
+          gfv[u][0] = fma(qm0, unm, -qp[u][0] * unp[u]);
+          gfv[u][1] = fma(dp, nx, fma(qm1, unm, -qp[u][1] * unp[u]));
+          gfv[u][2] = fma(dp, ny, fma(qm2, unm, -qp[u][2] * unp[u]));
+          gfv[u][3] = fma(dp, nz, fma(qm3, unm, -qp[u][3] * unp[u]));
+          gfv[u][4] = fma(qm4 + pm, unm, -(qp[u][4] + pp[u]) * unp[u]);
+          dqv[u][0] = qp[u][0] - qm0;
+          dqv[u][1] = qp[u][1] - qm1;
+          dqv[u][2] = qp[u][2] - qm2;
+          dqv[u][3] = qp[u][3] - qm3;
+          dqv[u][4] = qp[u][4] - qm4;
+        }
       }
       if (A.lambda_mode == 0) {
 #pragma unroll
@@ -1732,6 +1750,13 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         if (!act) continue;
         const int e = face >> 2, f = face & 3;
         const double* Gf = g_s + e * GEO + 9 + 4 * f;
+        double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
+        if (DG_HO_F1) {
+          const double hfs = 0.5 * Gf[3];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) xd[c * XS] = hfs * fma(lam[u], dqv[u][c], gfv[u][c]);
+          continue;
+        }
         const double nx = Gf[0], ny = Gf[1], nz = Gf[2], hfs = 0.5 * Gf[3];
         const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
         double qm[5];
@@ -1746,7 +1771,6 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         df[3] = fma(pdm, nz, qm[3] * unm) - fma(pdp, nz, qp[u][3] * unp[u]);
         df[4] = (qm[4] + pm) * unm - (qp[u][4] + pp[u]) * unp[u];
         // Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-))
-        double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
 #pragma unroll
         for (int c = 0; c < 5; ++c) xd[c * XS] = hfs * fma(lam[u], qp[u][c] - qm[c], df[c]);
       }
