@@ -863,6 +863,12 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #define DG_SDF 1
 #endif
     constexpr bool SDF = DG_SDF && W::GS > 0 && W::GS <= 4;
+    // DG_SCOL: the odd n-tile with one column per lane (t < GS) over the whole k-step instead of
+    // partial sums over the lane's k reduced afterwards; needs 16-byte aligned X rows and Op blocks
+#ifndef DG_SCOL   // measured slower: C3 63.3 vs 65.7, C4 53.3 vs 56.2 GDOF/s
+#define DG_SCOL 0
+#endif
+    constexpr bool SCOL = SDF && DG_SCOL && XSV % 2 == 0 && XSF % 2 == 0 && (W::NPG * 64) % 2 == 0 && W::OPW % 2 == 0;
     double sacc[NSING > 0 ? NSING : 1][4];
 #pragma unroll
     for (int k = 0; k < NSING; ++k) sacc[k][0] = sacc[k][1] = sacc[k][2] = sacc[k][3] = 0.0;
@@ -890,7 +896,23 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           dmma_8x8x4(acc[2 * k], a0, b.x);
           dmma_8x8x4(acc[2 * k + 1], a0, b.y);
         }
-        if (NSING > 0 && SDF) {
+        if (NSING > 0 && SCOL) {
+          // lane t owns column t of the odd n-tile: the 4 k of the k-step for its row (two 16-byte
+          // loads of the X row) against Op(col t, 4ks..4ks+3) (two 16-byte loads), two partial sums
+          const double* bo = ob + W::NPG * 64 + 4 * t4;
+          const double2 b01 = *reinterpret_cast<const double2*>(bo);
+          const double2 b23 = *reinterpret_cast<const double2*>(bo + 2);
+#pragma unroll
+          for (int k = 0; k < NSING; ++k) {
+            const double* xr = X + (mts[k] * 8 + g) * XSTR + (ks - XK0) * 4;
+            const double2 a01 = *reinterpret_cast<const double2*>(xr);
+            const double2 a23 = *reinterpret_cast<const double2*>(xr + 2);
+            sacc[k][0] = fma(a01.x, b01.x, sacc[k][0]);
+            sacc[k][1] = fma(a01.y, b01.y, sacc[k][1]);
+            sacc[k][0] = fma(a23.x, b23.x, sacc[k][0]);
+            sacc[k][1] = fma(a23.y, b23.y, sacc[k][1]);
+          }
+        } else if (NSING > 0 && SDF) {
           double bv[4];
 #pragma unroll
           for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
@@ -967,7 +989,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #ifndef DG_SRED2
 #define DG_SRED2 1
 #endif
-    if (SDF && DG_SRED2) {
+    if (SCOL) {   // lane t already holds column t (lanes t >= GS: padding, not stored)
+#pragma unroll
+      for (int k = 0; k < NSING; ++k) acc[2 * NPAIR + k][0] = sacc[k][0] + sacc[k][1];
+    } else if (SDF && DG_SRED2) {
       // sum the singles' partial products over the 4 lanes of a row, lane t keeping column t, as
       // a transposing butterfly (3 shuffles per single instead of 2 GS): step 1 (xor 1) each lane
       // keeps the columns of its parity, step 2 (xor 2) the one of its half; all singles' shuffles
