@@ -125,13 +125,8 @@ cudaError_t launch_stage(int N, const dgk::StageArgs& A, int max_ctas, cudaStrea
   switch (N) {
     case 1: return launch_ws_n<1, MODE>(A, max_ctas, st);
     case 2: return launch_ws_n<2, MODE>(A, max_ctas, st);
-#ifdef DG_HO34   // experiment: the phased kernel at N = 3, 4
-    case 3: return launch_ho_n<3, MODE>(A, max_ctas, st);
-    case 4: return launch_ho_n<4, MODE>(A, max_ctas, st);
-#else
     case 3: return launch_ws_n<3, MODE>(A, max_ctas, st);
     case 4: return launch_ws_n<4, MODE>(A, max_ctas, st);
-#endif
     case 5: return launch_ho_n<5, MODE>(A, max_ctas, st);
     case 6: return launch_ho_n<6, MODE>(A, max_ctas, st);
   }

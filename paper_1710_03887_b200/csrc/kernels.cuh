@@ -268,16 +268,15 @@ __device__ __forceinline__ void tma_store_commit_and_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
-template <int XSTR_, int K0_, int K1_, int XK0_ = K0_>
-struct KBlk {   // k-steps [K0, K1) of a block of X whose first column is k-step XK0
-  static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_, XK0 = XK0_;
+template <int XSTR_, int K0_, int K1_>
+struct KBlk {   // k-steps [K0, K1) of the X block that starts at k-step K0
+  static constexpr int XSTR = XSTR_, K0 = K0_, K1 = K1_;
 };
 
 // Neighbour traces of NPASS face passes (face of pass u: fbase + u fstride; one face per
 // SEGW-lane segment, lane i < NFP its node i): local neighbour / halo record gathers, or the
 // boundary ghost from the own trace; idle lanes keep a finite filler.
-// FMB = 0: face = 4 e + f (element-major); FMB = EB: face = f EB + e (face-major, DG_FSPLIT)
-template <int N, int NPASS, int FMB = 0>
+template <int N, int NPASS>
 __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                             bool lane_ok, const double* q_s, const double* g_s, const int* n_s,
                                             const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
@@ -295,7 +294,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 #pragma unroll
     for (int u = 0; u < NPASS; ++u) {
       const int face = fbase + u * fstride;
-      const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
+      const int e = face >> 2, f = face & 3;
       ok[u] = !DG_SKIPQ(2) && lane_ok && face < flim && e < ne;
       const int ec = ok[u] ? e : 0;
       code[u] = ok[u] ? int(c_s[ec * 4 + f]) : CODE_BC;
@@ -322,7 +321,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
         for (int c = 0; c < 5; ++c) qp[u][c] = __ldg(q2 + c * NFP);
       } else if (ok[u]) {   // boundary ghost from the own trace (Q of this tile is in shared memory)
         const int face = fbase + u * fstride;
-        const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
+        const int e = face >> 2, f = face & 3;
         const double* G = g_s + e * GEO + 9 + 4 * f;
         const double* q = q_s + e * 5 * NP + node[u];
         double qm[5];
@@ -331,12 +330,11 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
         ghost_trace(A, code[u] - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
       }
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
-    const int e = FMB ? face % FMB : face >> 2, f = FMB ? face / FMB : face & 3;
+    const int e = face >> 2, f = face & 3;
 #pragma unroll
     for (int c = 0; c < 5; ++c) qp[u][c] = A.qinf[c];
     if (!DG_SKIPQ(2) && lane_ok && face < flim && e < ne) {
@@ -353,6 +351,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
       }
     }
   }
+  }
 }
 
 // Face terms of NPASS passes into the face block of X (row stride XSF, column f Nfp + i):
@@ -362,7 +361,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 //   Fscale (n.F(q-) - F*) = Fscale/2 ((n.F(q-) - n.F(q+)) + lam (q+ - q-)),
 // where the ambient-pressure shift (A14) cancels in n.F(q-) - n.F(q+).  Slots of elements past
 // ne store zeros.
-template <int N, int NPASS, int SEGW, int XSF, int FMB = 0>
+template <int N, int NPASS, int SEGW, int XSF>
 __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                            bool lane_ok, const double* q_s, const double* g_s, const uint8_t* sFm,
                                            const double (&qp)[NPASS][5], double* sXf) {
@@ -382,9 +381,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
-    const bool act = lane_ok && face < flim && (FMB ? face % FMB : face >> 2) < ne;
+    const bool act = lane_ok && face < flim && (face >> 2) < ne;
     const int fc = act ? face : 0;
-    const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
+    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
     const double* G = g_s + e * GEO + 9 + 4 * f;
     const double nx = G[0], ny = G[1], nz = G[2];
     const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
@@ -446,9 +445,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
     for (int u = 0; u < NPASS; ++u) {
       const int face = fbase + u * fstride;
       const bool slot = lane_ok && face < flim;
-      const bool act = slot && (FMB ? face % FMB : face >> 2) < ne;
+      const bool act = slot && (face >> 2) < ne;
       const int fc = slot ? face : 0;
-      const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
+      const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
       const double hfs = act ? 0.5 * g_s[e * GEO + 9 + 4 * f + 3] : 0.0;
       double* xd = sXf + (e * 5) * XSF + f * NFP + ii;
       if (slot) {
@@ -461,9 +460,9 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
   for (int u = 0; u < NPASS; ++u) {
     const int face = fbase + u * fstride;
     const bool slot = lane_ok && face < flim;
-    const bool act = slot && (FMB ? face % FMB : face >> 2) < ne;
+    const bool act = slot && (face >> 2) < ne;
     const int fc = slot ? face : 0;
-    const int e = FMB ? fc % FMB : fc >> 2, f = FMB ? fc / FMB : fc & 3, ii = lane_ok ? i : 0;
+    const int e = fc >> 2, f = fc & 3, ii = lane_ok ? i : 0;
     const double* G = g_s + e * GEO + 9 + 4 * f;
     const double nx = G[0], ny = G[1], nz = G[2], hfs = act ? 0.5 * G[3] : 0.0;
     const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
@@ -530,42 +529,22 @@ template <int N>
 struct WS {
 #ifdef DG_WS_EB
   static constexpr int EB = DG_WS_EB;
-#elif defined(DG_WS_EB3)
-  static constexpr int EB = N == 3 ? DG_WS_EB3 : (N <= 2) ? 32 : 16;
-#elif defined(DG_WS_EB4)
-  static constexpr int EB = N == 4 ? DG_WS_EB4 : (N <= 2) ? 32 : 16;
 #else
   static constexpr int EB = (N <= 2) ? 32 : 16;
 #endif
   // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 3 the
   // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3)
-  // DG_SMR: 20 warps (12 producer + 8 consumer) with the register file re-split at run time
-  // (setmaxnreg): the kernel is compiled for R0 = 65536 / NT registers, consumer warps drop to
-  // CREG and producer warps rise to PREG, with CW (R0 - CREG) >= PW (PREG - R0) so the
-  // increase is served by the decrease
-#ifndef DG_SMR
-#define DG_SMR 0
-#endif
-  static constexpr bool SMR = DG_SMR && N >= 3;
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;
 #else
-  static constexpr int PW = SMR ? 12 : N == 3 ? 12 : 8;
+  static constexpr int PW = N == 3 ? 12 : 8;
 #endif
 #ifdef DG_WS_CW
   static constexpr int CW = DG_WS_CW;
 #else
-  static constexpr int CW = SMR ? 8 : N == 3 ? 4 : 8;
+  static constexpr int CW = N == 3 ? 4 : 8;
 #endif
   static constexpr int NT = 32 * (PW + CW);
-  static constexpr int R0 = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
-#ifdef DG_SMR_CREG
-  static constexpr int CREG = DG_SMR_CREG;
-#else
-  static constexpr int CREG = 72;
-#endif
-  static constexpr int PREG = R0 + (CW * (R0 - CREG) / PW) / 8 * 8;
-  static_assert(!SMR || (CW % 4 == 0 && PW % 4 == 0 && PREG >= R0 && PREG <= 248 && CREG >= 24), "register split");
   static constexpr int PT = 32 * PW, CT = 32 * CW;
   static constexpr int ROWS = 5 * EB;                       // multiple of 8 (DMMA m8 row tiles)
   static_assert(ROWS % 8 == 0, "rows must fill DMMA m8 tiles");
@@ -619,52 +598,7 @@ struct WS {
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
   static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
-                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9, BAR_CV = 10;
-  // DG_CTAIL (N = 4): the volume slots of the last, partial producer round (EB Np - (VR-1) PT
-  // = 48 nodes at N = 4) are computed by the two last consumer warps for the next tile, right
-  // after their volume contraction, so the producers' serial volume phase is one round shorter
-#ifndef DG_CTAIL   // measured slower: C4 53.3 vs 55.6 GDOF/s (the two-round volume phase took as long)
-#define DG_CTAIL 0
-#endif
-  static constexpr int VR = (EB * Shape<N>::NP + PT - 1) / PT;
-  static constexpr int TAILN = EB * Shape<N>::NP - (VR - 1) * PT;
-  static constexpr bool CTAIL = DG_CTAIL && N == 4 && VR >= 2 && TAILN > 0 && TAILN <= 64 && CW >= 2;
-  static constexpr int CT0 = (CW - 2) * 32;   // first consumer thread of the tail
-  // DG_PODD (N = 3): the odd trailing n-tile (4 node columns) is contracted by the producers --
-  // on DMMA, one 8-row tile per producer warp, after their face phase -- together with its part
-  // of the epilogue; the consumers keep only the n-tile pairs.  C3 is consumer-bound (the
-  // producers idle at XV_EMPTY), so this moves work to the side that waits.
-#ifndef DG_PODD   // measured slower: C3 47.9 vs 64.8 GDOF/s (the producers' chain becomes the bound)
-#define DG_PODD 0
-#endif
-  static constexpr bool PODD = DG_PODD && N == 3 && HS && PW >= ROWS / 8;
-  static constexpr int BARC_N = CT + (PODD ? PT : 0);   // threads meeting at BAR_C
-  // DG_CHI: consumers take the HIGH warp ids (the SMSP arbiter favours them), producers the low
-  // ones; the SMSP of consumer warp cw stays cw % 4 (PW % 4 == 0)
-#ifndef DG_CHI
-#define DG_CHI 0
-#endif
-  static constexpr bool CHI = DG_CHI && PW % 4 == 0;
-  // DG_PEPI (N = 3, deep buffering): the epilogue is split -- the consumers form res = a res +
-  // dt rhs in place (their only shared-memory pass) and arrive on BAR_E; the producers, who wait
-  // at this point anyway on C3, form Q += b res over the whole tile with conflict-free
-  // contiguous accesses, issue both bulk stores and all residual loads, and reuse the buffers
-  // in program order (no BAR_C, no Q_EMPTY) -- the consumers go straight to the next tile
-#ifndef DG_PEPI   // measured slower: C3 62.2 vs 64.8 GDOF/s
-#define DG_PEPI 0
-#endif
-  static constexpr bool PEPI = DG_PEPI && N == 3 && DEEP && !PODD;
-  static constexpr int BAR_E = 11;
-  // DG_FSPLIT (N = 4): faces in face-major order (pass u = face u of every element); the face
-  // block's first k-steps (faces 0 and 1: 2 Nfp columns) are released after the first two
-  // passes (BAR_XF_FULL), the rest after the last two (BAR_XF_FULL_B), so the consumers' face
-  // contraction starts half a face phase earlier
-#ifndef DG_FSPLIT   // measured slower: C4 53.5 vs 56.1 GDOF/s (two face passes per half lose ILP)
-#define DG_FSPLIT 0
-#endif
-  static constexpr bool FSPLIT = DG_FSPLIT && N == 4 && !FDENSE && NSEG * PW == EB && FPASS == 4;
-  static constexpr int BAR_XF_FULL_B = 12;
-  static constexpr int KSPLIT = Shape<N>::KSV + (2 * Shape<N>::NFP) / 4;   // last k-step needing faces 0, 1 only (+1)
+                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9;
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -707,14 +641,11 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0)
 #ifndef DG_SBV
 #define DG_SBV 0
 #endif
-#ifndef DG_STIE
-#define DG_STIE 0
-#endif
 template <int N>
 struct M8Plan {
   static constexpr int MT8 = WS<N>::ROWS / 8;
   static constexpr int NPG = WS<N>::NPG, HS = WS<N>::HS;
-  static constexpr int P = MT8 * NPG, SG = WS<N>::PODD ? 0 : MT8 * HS, CW = WS<N>::CW;
+  static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N>::CW;
   static constexpr int CPMAX = (P + CW - 1) / CW;
   static constexpr bool SDF1 = WS<N>::GS > 0 && WS<N>::GS <= 4;
 #ifdef DG_SWSI
@@ -737,12 +668,10 @@ struct M8Plan {
       int best = 0;
       for (int w = 1; w < CW; ++w) {
         const int cb = WSI + (ns[best] ? 0 : SBV), cc = WSI + (ns[w] ? 0 : SBV);
-        // with a B-load term, ties go to a warp that already loads the odd tile's B values;
-        // DG_STIE: remaining ties go to the later warp (fewer pairs: the singles' reduction and
-        // epilogue then stay off the warps with the longest contraction)
+        // with a B-load term, ties go to a warp that already loads the odd tile's B values
         const int a = ((smsp[w % 4] + cc) * 4096 + load[w] + cc) * 2 + (SBV > 0 && ns[w] == 0);
         const int b = ((smsp[best % 4] + cb) * 4096 + load[best] + cb) * 2 + (SBV > 0 && ns[best] == 0);
-        if (a < b || (DG_STIE && a == b)) best = w;
+        if (a < b) best = w;
       }
       const int c = WSI + (ns[best] ? 0 : SBV);
       load[best] += c;
@@ -837,15 +766,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     tma_load_1d(ib + W::BQ + W::BG, A.nbr + size_t(e0) * 4, W::BN, io.barIn + b);
     tma_load_1d(ib + W::BQ + W::BG + W::BN, A.code + size_t(e0) * 4, W::BC, io.barIn + b);
   };
-  // DG_EPI=1 (experiment): the epilogue stores res and Q_new straight from registers to global
-  // memory; nothing is written back to shared memory, so no consumer barrier and no bulk store
-  // close the tile.  The tile's shared buffers (input, residual) are released one tile later,
-  // after the next XV_FULL barrier, which every consumer warp passes only after its epilogue.
-#ifndef DG_EPI   // measured slower: C4 50.7 vs 55.6, C3 60.6 vs 61.4 GDOF/s (uncoalesced row-fragment stores)
-#define DG_EPI 0
-#endif
-  constexpr bool EPI = DG_EPI && MODE == MODE_UPDATE;
-  if (MODE == MODE_UPDATE && !W::PEPI && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
+  if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
   for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     const int e0 = A.e_begin + tile * EB;
@@ -863,12 +784,6 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #define DG_SDF 1
 #endif
     constexpr bool SDF = DG_SDF && W::GS > 0 && W::GS <= 4;
-    // DG_SCOL: the odd n-tile with one column per lane (t < GS) over the whole k-step instead of
-    // partial sums over the lane's k reduced afterwards; needs 16-byte aligned X rows and Op blocks
-#ifndef DG_SCOL   // measured slower: C3 63.3 vs 65.7, C4 53.3 vs 56.2 GDOF/s
-#define DG_SCOL 0
-#endif
-    constexpr bool SCOL = SDF && DG_SCOL && XSV % 2 == 0 && XSF % 2 == 0 && (W::NPG * 64) % 2 == 0 && W::OPW % 2 == 0;
     double sacc[NSING > 0 ? NSING : 1][4];
 #pragma unroll
     for (int k = 0; k < NSING; ++k) sacc[k][0] = sacc[k][1] = sacc[k][2] = sacc[k][3] = 0.0;
@@ -881,8 +796,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       return unit_nt(u) * 8 + 2 * t4 + q;
     };
     auto kloop = [&](auto xblk) {
-      constexpr int XSTR = decltype(xblk)::XSTR, K1 = decltype(xblk)::K1, XK0 = decltype(xblk)::XK0;
-      constexpr int K0 = decltype(xblk)::K0;
+      constexpr int XSTR = decltype(xblk)::XSTR, K0 = decltype(xblk)::K0, K1 = decltype(xblk)::K1;
       if DG_SKIPQ(1) return;
       const double* X = (K0 == 0) ? io.sXv : io.sXf;
       constexpr int KU = kunroll<N>();
@@ -891,34 +805,18 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         const double* ob = io.sOp + ks * W::OPW;
 #pragma unroll
         for (int k = 0; k < NPAIR; ++k) {
-          const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
+          const double a0 = X[(mtp[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
           const double2 b = *reinterpret_cast<const double2*>(ob + (ntp[k] >> 1) * 64 + 2 * lane);
           dmma_8x8x4(acc[2 * k], a0, b.x);
           dmma_8x8x4(acc[2 * k + 1], a0, b.y);
         }
-        if (NSING > 0 && SCOL) {
-          // lane t owns column t of the odd n-tile: the 4 k of the k-step for its row (two 16-byte
-          // loads of the X row) against Op(col t, 4ks..4ks+3) (two 16-byte loads), two partial sums
-          const double* bo = ob + W::NPG * 64 + 4 * t4;
-          const double2 b01 = *reinterpret_cast<const double2*>(bo);
-          const double2 b23 = *reinterpret_cast<const double2*>(bo + 2);
-#pragma unroll
-          for (int k = 0; k < NSING; ++k) {
-            const double* xr = X + (mts[k] * 8 + g) * XSTR + (ks - XK0) * 4;
-            const double2 a01 = *reinterpret_cast<const double2*>(xr);
-            const double2 a23 = *reinterpret_cast<const double2*>(xr + 2);
-            sacc[k][0] = fma(a01.x, b01.x, sacc[k][0]);
-            sacc[k][1] = fma(a01.y, b01.y, sacc[k][1]);
-            sacc[k][0] = fma(a23.x, b23.x, sacc[k][0]);
-            sacc[k][1] = fma(a23.y, b23.y, sacc[k][1]);
-          }
-        } else if (NSING > 0 && SDF) {
+        if (NSING > 0 && SDF) {
           double bv[4];
 #pragma unroll
           for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
-            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
+            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
 #pragma unroll
             for (int c = 0; c < W::GS; ++c) sacc[k][c] = fma(a0, bv[c], sacc[k][c]);
           }
@@ -926,7 +824,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
           const double bs = lane < 4 * W::GS ? ob[W::NPG * 64 + lane] : 0.0;
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
-            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - XK0) * 4];
+            const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
             dmma_8x8x4(acc[2 * NPAIR + k], a0, bs);
           }
         }
@@ -935,64 +833,25 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     if (io.ctid < 32) trace_ev(A, j, 0);
     nbar_sync(W::BAR_XV_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 1);
-    if (EPI) {
-      // every consumer warp has finished tile j-1's epilogue (it passed XV_FULL after it): its
-      // input and residual buffers are free
-      if (io.ctid == IOT) {
-        if (W::NRES == 1 && j >= 1 && ne == EB) load_res(j);
-        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) load_res(j + 1);
-        if (W::NIN == 2 && j >= 1 && j + 1 < io.nmine && tile_full(j + 1)) fetch_in(j + 1);
-      }
-      if ((io.ctid >> 5) == IOW && j >= 1) {
-        const int pbuf = (j - 1) % W::NIN;
-        if ((W::NIN == 2 && j + 1 < io.nmine && !tile_full(j + 1)) || (W::NIN > 2 && j - 1 + W::NIN < io.nmine)) {
-          __syncwarp();
-          nbar_arrive(W::BAR_Q_EMPTY + pbuf, W::PT + 32);
-        }
-      }
-    } else if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
+    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
       // tile j-1's residual store has left sRes by now (issued at the end of its epilogue)
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       load_res(j);
     }
     kloop(KBlk<XSV, 0, S::KSV>{});
     if (io.ctid < 32) trace_ev(A, j, 2);
-    if constexpr (W::CTAIL) {
-      if (j + 1 < io.nmine) {
-        nbar_sync(W::BAR_CV, W::CT);   // every consumer warp is done reading Xv(j)
-        nbar_arrive(W::BAR_XV_EMPTY, NT);
-        if (io.ctid >= W::CT0 && io.ctid < W::CT0 + W::TAILN && tile_full(j + 1)) {
-          const int b1 = (j + 1) % W::NIN;
-          mbar_wait(io.barIn + b1, ((j + 1) / W::NIN) & 1);
-          const unsigned char* ib = io.in0 + b1 * W::BIN;
-          vol_node<N, XSV>(A, (W::VR - 1) * W::PT + io.ctid - W::CT0, reinterpret_cast<const double*>(ib),
-                           reinterpret_cast<const double*>(ib + W::BQ), e0 + EB * int(gridDim.x), EB, A.gamma - 1.0,
-                           io.sXv, EB * NP);
-        }
-      }
-    } else {
-      if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
-    }
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
 
     nbar_sync(W::BAR_XF_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 3);
-    if constexpr (W::FSPLIT) {
-      kloop(KBlk<XSF, S::KSV, W::KSPLIT, S::KSV>{});
-      nbar_sync(W::BAR_XF_FULL_B, NT);
-      kloop(KBlk<XSF, W::KSPLIT, S::KS4, S::KSV>{});
-    } else {
-      kloop(KBlk<XSF, S::KSV, S::KS4>{});
-    }
+    kloop(KBlk<XSF, S::KSV, S::KS4>{});
     if (io.ctid < 32) trace_ev(A, j, 4);
     trace_w(A, j, 0);
     if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
 #ifndef DG_SRED2
 #define DG_SRED2 1
 #endif
-    if (SCOL) {   // lane t already holds column t (lanes t >= GS: padding, not stored)
-#pragma unroll
-      for (int k = 0; k < NSING; ++k) acc[2 * NPAIR + k][0] = sacc[k][0] + sacc[k][1];
-    } else if (SDF && DG_SRED2) {
+    if (SDF && DG_SRED2) {
       // sum the singles' partial products over the 4 lanes of a row, lane t keeping column t, as
       // a transposing butterfly (3 shuffles per single instead of 2 GS): step 1 (xor 1) each lane
       // keeps the columns of its parity, step 2 (xor 2) the one of its half; all singles' shuffles
@@ -1051,7 +910,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             const int n = unit_n(u, q);
             const int li = (unit_mt(u) * 8 + g) * NP + (n < NP ? n : 0);
             rv[u - u0][q] = sRes[li];
-            if (!W::PEPI) qv[u - u0][q] = q_s[li];
+            qv[u - u0][q] = q_s[li];
           }
 #pragma unroll
         for (int u = u0; u < u0 + CH && u < NSLOT; ++u)
@@ -1061,19 +920,9 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             if (n >= NP) continue;
             const int li = (unit_mt(u) * 8 + g) * NP + n;   // == (e*5 + c)*NP + n
             const double rr = fma(A.a, rv[u - u0][q], A.dt * acc[u][q]);
-            if (W::PEPI) {
-              sRes[li] = rr;
-              continue;
-            }
             const double qn = fma(A.b, rr, qv[u - u0][q]);
-            if (EPI) {
-              const size_t gi = size_t(e0) * 5 * NP + li;
-              A.res[gi] = rr;
-              A.Qout[gi] = qn;
-            } else {
-              sRes[li] = rr;
-              q_s[li] = qn;
-            }
+            sRes[li] = rr;
+            q_s[li] = qn;
           }
       }
     } else {
@@ -1101,18 +950,11 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
     if (io.ctid < 32) trace_ev(A, j, 6);
     trace_w(A, j, 1);
-    if (EPI) continue;   // buffers are released after the next XV_FULL (above)
-    if constexpr (W::PEPI) {
-      if (staged) nbar_arrive(W::BAR_E, W::CT + W::PT);   // the producers finish the tile
-      continue;
-    }
     if (staged) {
       // every thread that wrote the staged tiles orders its generic-proxy stores before the
       // async-proxy (TMA) reads of the bulk stores issued after the barrier
-#ifndef DG_EXP_NOFENCE
       fence_proxy_async();
-#endif
-      nbar_sync(W::BAR_C, W::BARC_N);
+      nbar_sync(W::BAR_C, W::CT);
       if (io.ctid < 32) trace_ev(A, j, 7);
       if (io.ctid == IOT) {
         // Q first: once its bulk read is done the input buffer is free; the residual store is
@@ -1189,13 +1031,9 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 
   // Producers take the HIGH warp ids: the SMSP arbiter issues highest-wid-first, so their
   // short FP64 chains win the shared FP64/DMMA pipe and the consumers fill the remaining slots.
-  const bool is_producer = W::CHI ? warp < W::PW : warp >= W::CW;
-  if constexpr (W::SMR) {
-    if (is_producer) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(W::PREG));
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(W::CREG));
-  }
+  const bool is_producer = warp >= W::CW;
   if (is_producer) {
-    const int ptid = W::CHI ? tid : tid - W::CT, pwarp = ptid >> 5;
+    const int ptid = tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
     const double gm1 = A.gamma - 1.0;
     auto fetch = [&](int jj) {
@@ -1226,38 +1064,6 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
         nbar_sync(W::BAR_P, PT);
       }
     };
-    // PEPI: the second half of tile jm's epilogue and its bulk stores (called once the consumers
-    // are through with the tile); the stores of tile jm - 1 are waited for first, which frees
-    // residual buffer (jm - 1) % 2 for tile jm + 1 and input buffer (jm - 1) % 3 for tile jm + 2
-    auto staged_t = [&](int jj) {
-      return MODE == MODE_UPDATE && A.e_end - (A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB) >= EB;
-    };
-    auto res_load = [&](int jj) {   // one thread
-      const int e0r = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&sBar[W::NIN + jj % W::NRES], W::BQ);
-      tma_load_1d(sRes + (jj % W::NRES) * (W::BQ / 8), A.res + size_t(e0r) * 5 * NP, W::BQ, &sBar[W::NIN + jj % W::NRES]);
-    };
-    auto pepi = [&](int jm) {
-      nbar_sync(W::BAR_E, W::CT + W::PT);
-      double* qw = bufQ(jm % W::NIN);
-      const double* rw = sRes + (jm % W::NRES) * (W::BQ / 8);
-      for (int li = ptid; li < EB * 5 * NP; li += PT) qw[li] = fma(A.b, rw[li], qw[li]);
-      fence_proxy_async();
-      nbar_sync(W::BAR_P, PT);
-      if (ptid == 0) {
-        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        if (jm + 1 < nmine && staged_t(jm + 1)) res_load(jm + 1);
-        const int e0m = A.e_begin + (int(blockIdx.x) + jm * int(gridDim.x)) * EB;
-        fence_proxy_async();
-        tma_store_1d(A.Qout + size_t(e0m) * 5 * NP, qw, W::BQ);
-        tma_store_1d(A.res + size_t(e0m) * 5 * NP, rw, W::BQ);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      }
-    };
-    if constexpr (W::PEPI) {
-      if (ptid == 0 && nmine > 0 && staged_t(0)) res_load(0);
-    }
     if (nmine > 0) fetch(0);
     if (W::NIN == 2 && nmine > 1) fetch(1);   // later full tiles are fetched by the consumers
     for (int j = 0; j < nmine; ++j) {
@@ -1278,11 +1084,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const bool lane_ok = i < NFP && seg < W::NSEG;
       const int fbase = pwarp * W::NSEG + seg;
       double qp[W::FPASS][5];
-#ifndef DG_GLATE   // experiment: issue the gathers after the volume phase
-#define DG_GLATE 0
-#endif
-      constexpr int FMB = W::FSPLIT ? EB : 0;
-      if (!DG_GLATE) face_gather<N, W::FPASS, FMB>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
+      face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
@@ -1306,9 +1108,6 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           if constexpr (SKIPV) {
             if (rr * PT + (W::PW - 1 - pwarp) * 32 >= EB * NP) continue;
           }
-          if constexpr (W::CTAIL) {
-            if (rr == VR - 1 && j > 0 && ne == EB) continue;   // the consumers computed it
-          }
           const int idx = SKIPV ? (W::PW - 1 - pwarp) * 32 + lane + rr * PT : ptid + rr * PT;
           vol_node<N, XSV>(A, idx, q_s, g_s, e0, ne, gm1, sXv, EB * NP);
         }
@@ -1324,100 +1123,25 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
           fetch(j + 1);
         }
       } else if (j + 1 < nmine) {
-        if (j + 1 >= W::NIN) {
-          if constexpr (W::PEPI) {
-            // the buffer's last user, tile j-2, left by bulk stores issued by thread 0 (pepi):
-            // thread 0 waits for their reads; the partial-tile path of fetch writes with every
-            // producer thread, so they meet thread 0 first
-            if (ptid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-            if (A.e_end - (A.e_begin + (int(blockIdx.x) + (j + 1) * int(gridDim.x)) * EB) < EB) nbar_sync(W::BAR_P, PT);
-          } else {
-            nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
-          }
-        }
+        if (j + 1 >= W::NIN) nbar_sync(W::BAR_Q_EMPTY + (j + 1) % W::NIN, W::PT + 32);
         fetch(j + 1);
       }
       // ---- face fluxes -> Xf
-      if (DG_GLATE) face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 12);
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
-      if constexpr (W::PEPI) {
-        if (j >= 1 && staged_t(j - 1)) pepi(j - 1);
-      }
       if (ptid < 32) trace_ev(A, j, 13);
-      if constexpr (W::FSPLIT) {
-        using QP2 = const double(&)[2][5];
-        face_terms<N, 2, W::SEGW, XSF, FMB>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm,
-                                            reinterpret_cast<QP2>(qp[0]), sXf);
-        nbar_arrive(W::BAR_XF_FULL, NT);
-        face_terms<N, 2, W::SEGW, XSF, FMB>(A, fbase + 2 * W::PW * W::NSEG, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s,
-                                            g_s, sFm, reinterpret_cast<QP2>(qp[2]), sXf);
-        if (ptid < 32) trace_ev(A, j, 14);
-        trace_w(A, j, 1);
-        nbar_arrive(W::BAR_XF_FULL_B, NT);
-      } else {
-        face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
-        if (ptid < 32) trace_ev(A, j, 14);
-        trace_w(A, j, 1);
-        nbar_arrive(W::BAR_XF_FULL, NT);
-      }
-      if constexpr (W::PODD) {
-        // ---- the odd n-tile of tile j: X complete once every producer warp is past its face terms
-        nbar_sync(W::BAR_P, PT);
-        const bool staged = MODE == MODE_UPDATE && ne == EB;
-        if (pwarp < W::ROWS / 8 && !DG_SKIPQ(1)) {
-          const int g = lane >> 2, t4 = lane & 3, row = pwarp * 8 + g;
-          double acc[2] = {0.0, 0.0};
-          const double* bo = sOp + W::NPG * 64 + lane;
-          const bool bl = lane < 4 * W::GS;
-#pragma unroll 5
-          for (int ks = 0; ks < S::KSV; ++ks)
-            dmma_8x8x4(acc, sXv[row * XSV + 4 * ks + t4], bl ? bo[ks * W::OPW] : 0.0);
-#pragma unroll 5
-          for (int ks = S::KSV; ks < S::KS4; ++ks)
-            dmma_8x8x4(acc, sXf[row * XSF + 4 * (ks - S::KSV) + t4], bl ? bo[ks * W::OPW] : 0.0);
-          if (staged) mbar_wait(&sBar[W::NIN + j % W::NRES], (j / W::NRES) & 1);
-          double* qw = bufQ(buf);
-          double* rw = sRes + (j % W::NRES) * (W::BQ / 8);
-          const int e = row / 5, c = row - 5 * e;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int cn = 2 * t4 + q;
-            if (cn >= W::GS) continue;
-            const int n = (S::NTL - 1) * 8 + cn, li = row * NP + n;
-            if (staged) {
-              const double rr = fma(A.a, rw[li], A.dt * acc[q]);
-              rw[li] = rr;
-              qw[li] = fma(A.b, rr, qw[li]);
-            } else if (e < ne) {
-              if (MODE == MODE_UPDATE) {
-                const size_t gi = size_t(e0) * 5 * NP + li;
-                const double rr = fma(A.a, __ldg(A.res + gi), A.dt * acc[q]);
-                A.res[gi] = rr;
-                A.Qout[gi] = fma(A.b, rr, qw[li]);
-              } else {
-                A.out[(size_t(c) * A.Kpub + A.pub[e0 + e]) * NP + n] = acc[q];
-              }
-            }
-          }
-        }
-        if (staged) {   // the consumers' bulk stores of the tile wait for these columns too
-          fence_proxy_async();
-          nbar_arrive(W::BAR_C, W::BARC_N);
-        }
-      }
-    }
-    if constexpr (W::PEPI) {
-      if (nmine > 0 && staged_t(nmine - 1)) pepi(nmine - 1);
-      if (ptid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete before exit
+      face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
+      if (ptid < 32) trace_ev(A, j, 14);
+      trace_w(A, j, 1);
+      nbar_arrive(W::BAR_XF_FULL, NT);
     }
   } else {
     // ======================= consumers: DMMA contraction + LSERK epilogue
     // every warp runs a compile-time-shaped loop over its units so its DMMA chains interleave
     // without run-time branches
     using PL = M8Plan<N>;
-    const int cw = W::CHI ? warp - W::PW : warp;
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, W::CHI ? tid - W::PT : tid, lane};
+    const int cw = warp;
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
@@ -1452,9 +1176,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 template <int N>
 struct HO {
   using S = Shape<N>;
-  // EB 16 at N <= 4 serves only the DG_HO34 experiment (the phased kernel at N = 3, 4 measured
-  // 38 GDOF/s on C3 and C4 against 64.8 / 55.9 for the warp-specialised kernel)
-  static constexpr int EB = N <= 4 ? 16 : 8, NW = 15, CT = 32 * NW, NT = CT + 32;   // + one loader warp
+  static constexpr int EB = 8, NW = 15, CT = 32 * NW, NT = CT + 32;   // + one loader warp
   static constexpr int ROWS = 5 * EB, MT8 = ROWS / 8;
   static constexpr int XS = S::XS;
   static constexpr int NPG = S::NTL / 2, HS = S::NTL % 2;
@@ -1715,13 +1437,10 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
       }
     }
     if (warp == 0) trace_ev(A, j, 4);
-    // ---- face terms -> X[:, KVP:KVP+4Nfp)  (DG_HO_F1: the own trace read once, as at N <= 4)
-#ifndef DG_HO_F1   // measured slower at N = 6: C5 23.7 vs 28.4 GDOF/s (32 B of spills)
-#define DG_HO_F1 0
-#endif
+    // ---- face terms -> X[:, KVP:KVP+4Nfp)  (the single-read form of the N <= 4 kernel spills
+    //      here: C5 23.7 vs 28.4 GDOF/s)
     if (!DG_SKIPQ(2)) {
       double rip[H::FPASS], unp[H::FPASS], pp[H::FPASS], lam[H::FPASS], unmv[H::FPASS], pmv[H::FPASS];
-      double dqv[DG_HO_F1 ? H::FPASS : 1][5], gfv[DG_HO_F1 ? H::FPASS : 1][5];
 #pragma unroll
       for (int u = 0; u < H::FPASS; ++u) {
         const int face = warp * H::NSEG + u * H::STRIDE + seg;
@@ -1742,20 +1461,6 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         pp[u] = gm1 * (qp[u][4] - 0.5 * (qp[u][1] * qp[u][1] + qp[u][2] * qp[u][2] + qp[u][3] * qp[u][3]) * rip[u]);
         const double l = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp[u]) + sqrt_nr(gamma * pp[u] * rip[u]));
         lam[u] = act ? l : 0.0;
-        if (DG_HO_F1) {
-          // n.F(q-) - n.F(q+): the ambient-pressure shift cancels (A14)
-          const double dp = pm - pp[u];
-          gfv[u][0] = fma(qm0, unm, -qp[u][0] * unp[u]);
-          gfv[u][1] = fma(dp, nx, fma(qm1, unm, -qp[u][1] * unp[u]));
-          gfv[u][2] = fma(dp, ny, fma(qm2, unm, -qp[u][2] * unp[u]));
-          gfv[u][3] = fma(dp, nz, fma(qm3, unm, -qp[u][3] * unp[u]));
-          gfv[u][4] = fma(qm4 + pm, unm, -(qp[u][4] + pp[u]) * unp[u]);
-          dqv[u][0] = qp[u][0] - qm0;
-          dqv[u][1] = qp[u][1] - qm1;
-          dqv[u][2] = qp[u][2] - qm2;
-          dqv[u][3] = qp[u][3] - qm3;
-          dqv[u][4] = qp[u][4] - qm4;
-        }
       }
       if (A.lambda_mode == 0) {
 #pragma unroll
@@ -1776,12 +1481,6 @@ __global__ void __launch_bounds__(HO<N>::NT, 1) stage_ho_kernel(const StageArgs 
         const int e = face >> 2, f = face & 3;
         const double* Gf = g_s + e * GEO + 9 + 4 * f;
         double* xd = sX + (e * 5) * XS + S::KVP + f * NFP + i;
-        if (DG_HO_F1) {
-          const double hfs = 0.5 * Gf[3];
-#pragma unroll
-          for (int c = 0; c < 5; ++c) xd[c * XS] = hfs * fma(lam[u], dqv[u][c], gfv[u][c]);
-          continue;
-        }
         const double nx = Gf[0], ny = Gf[1], nz = Gf[2], hfs = 0.5 * Gf[3];
         const double* q = q_s + e * 5 * NP + sFm[f * NFP + i];
         double qm[5];

@@ -56,12 +56,9 @@ struct MT {
   // the k range of each unit is split KP ways so every warp gets work; the KP partial results go
   // to separate buffers (in the neighbours' coefficient region, dead by then) and are summed in a
   // fixed order -- deterministic
-  // (DG_MKP=1: measured slower, p = 1 / 2 / 3: 16.9 / 12.3 / 9.5 vs 19.2 / 13.5 / 9.7 GDOF/s)
-#ifdef DG_MKP
-  static constexpr int KP = (64 + UNITS - 1) / UNITS < 4 ? (64 + UNITS - 1) / UNITS : 4;
-#else
+  // (k-split 2-4 ways so every warp gets a unit measured slower, p = 1 / 2 / 3: 16.9 / 12.3 / 9.5
+  // vs 19.2 / 13.5 / 9.7 GDOF/s)
   static constexpr int KP = 1;
-#endif
   // interpolation to the volume points on DMMA: A = the tile's coefficients as loaded ([row][NP];
   // k past NP meets zero B rows -- the values read there are the next row's coefficients or the
   // geometry behind the block, finite), n = point (NQ padded to NTQ tiles), result into the FS
