@@ -49,7 +49,7 @@ def up_to_date() -> bool:
 
 def defines() -> dict:
     """Compile-time tuning knobs from the environment (DG_WS_PW=...), for experiments."""
-    return {k: os.environ[k] for k in ("DG_WS_PW", "DG_WS_CW", "DG_WS_EB", "DG_HO_KC", "DG_HO_SLOTS", "DG_SDF", "DG_TRACE", "DG_KUNROLL", "DG_NEWTON2", "DG_HO_SDF", "DG_WS_IOW", "DG_SKIP_VOL", "DG_XSV4", "DG_FDENSE", "DG_F1", "DG_SBV", "DG_SWSI", "DG_GATHER2", "DG_SRED2", "DG_ECH", "DG_MODAL_TILE", "DG_MI", "DG_MFP", "DG_DEBUG_SKIP") if k in os.environ}
+    return {k: os.environ[k] for k in ("DG_WS_PW", "DG_WS_CW", "DG_WS_EB", "DG_HO_KC", "DG_HO_SLOTS", "DG_SDF", "DG_TRACE", "DG_KUNROLL", "DG_NEWTON2", "DG_HO_SDF", "DG_WS_IOW", "DG_SKIP_VOL", "DG_XSV4", "DG_FDENSE", "DG_F1", "DG_SBV", "DG_SWSI", "DG_GATHER2", "DG_SRED2", "DG_ECH", "DG_MODAL_TILE", "DG_MI", "DG_MFP", "DG_DEBUG_SKIP", "DG_IODEFER", "DG_CHI") if k in os.environ}
 
 
 def build(force: bool = False, verbose_ptxas: bool = False, out: str = LIB, extra_defines=None) -> str:

@@ -116,13 +116,13 @@ __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   }
 }
 
-// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*4 + k (k < 4), tiles < 48
+// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*8 + k (k < 8), tiles < 24
 __device__ __forceinline__ void trace_w(const StageArgs& A, int j, int k) {
-  if (DG_TRACE && blockIdx.x == 0 && j < 48 && A.trace) {
+  if (DG_TRACE && blockIdx.x == 0 && j < 24 && A.trace) {
     __syncwarp();
     unsigned long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 4 + k] = t;
+    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 8 + k] = t;
   }
 }
 
@@ -742,6 +742,14 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
   constexpr int IOW = W::CW - 1;
 #endif
   constexpr int IOT = 32 * IOW;
+  // IODEFER: the IO thread does not wait for a tile's bulk-store reads at the end of its
+  // epilogue; the input refill / release and (NRES == 1) the residual load follow at the next
+  // tile's XV_FULL
+#ifdef DG_IODEFER
+  constexpr bool IODEFER = DG_IODEFER;
+#else
+  constexpr bool IODEFER = N == 3;   // C3 66.0 -> 66.3 GDOF/s; at N = 4 (producers the bound) 56.0 -> 54.6
+#endif
   auto tile_full = [&](int jj) {
     const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
     return A.e_end - e0 >= EB;
@@ -812,8 +820,17 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         }
         if (NSING > 0 && SDF) {
           double bv[4];
+          if constexpr (W::GS == 4) {
+            // [t][c] layout (mesh.cpp, N <= 4): the lane's four columns in two 16-byte loads instead
+            // of four 8-byte ones (C3 65.5 -> 66.0, C2 54.5 -> 55.1 GDOF/s; at N = 6 the phased
+            // kernel measured slower with it, 28.4 -> 27.3, and keeps the [c][t] layout)
+            const double2 b01 = *reinterpret_cast<const double2*>(ob + W::NPG * 64 + 4 * t4);
+            const double2 b23 = *reinterpret_cast<const double2*>(ob + W::NPG * 64 + 4 * t4 + 2);
+            bv[0] = b01.x, bv[1] = b01.y, bv[2] = b23.x, bv[3] = b23.y;
+          } else {
 #pragma unroll
-          for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
+            for (int c = 0; c < W::GS; ++c) bv[c] = ob[W::NPG * 64 + 4 * c + t4];   // Op(32+c, 4ks+t)
+          }
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
             const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
@@ -821,7 +838,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
             for (int c = 0; c < W::GS; ++c) sacc[k][c] = fma(a0, bv[c], sacc[k][c]);
           }
         } else if (NSING > 0) {
-          const double bs = lane < 4 * W::GS ? ob[W::NPG * 64 + lane] : 0.0;
+          const double bs = lane < 4 * W::GS ? ob[W::NPG * 64 + (W::GS == 4 ? 4 * t4 + g : lane)] : 0.0;
 #pragma unroll
           for (int k = 0; k < NSING; ++k) {
             const double a0 = X[(mts[k] * 8 + g) * XSTR + t4 + (ks - K0) * 4];
@@ -831,9 +848,34 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       }
     };
     if (io.ctid < 32) trace_ev(A, j, 0);
+    trace_w(A, j, 4);
     nbar_sync(W::BAR_XV_FULL, NT);
+    trace_w(A, j, 5);
     if (io.ctid < 32) trace_ev(A, j, 1);
-    if (W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
+    if (IODEFER && j >= 1) {
+      // tile j-1's buffer hand-offs, deferred from the end of its epilogue to here: the bulk
+      // stores' shared-memory reads drain at the SM's share of the HBM write bandwidth (~1.4k
+      // cycles for the Q tile at N = 4), and a wait there held every consumer warp at XV_FULL
+      const int jp = j - 1, bufp = jp % W::NIN;
+      if (io.ctid == IOT) {
+        if (MODE == MODE_UPDATE) {
+          // NRES == 1: tile j-1's residual store must have left sRes too; else only its Q store
+          if (W::NRES == 1) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          if (W::NRES == 1 && ne == EB) load_res(j);
+        }
+        // two input buffers: refill the one tile j-1 used with the inputs of tile j+1
+        if (W::NIN == 2 && jp + 2 < io.nmine && tile_full(jp + 2)) fetch_in(jp + 2);
+      }
+      // the buffer is free: signal the producers (the partial last tile with two buffers, every
+      // tile with three)
+      if ((W::NIN == 2 ? (jp + 2 < io.nmine && !tile_full(jp + 2)) : (jp + W::NIN < io.nmine)) &&
+          (io.ctid >> 5) == IOW) {
+        __syncwarp();
+        nbar_arrive(W::BAR_Q_EMPTY + bufp, W::PT + 32);
+      }
+    }
+    if (!IODEFER && W::NRES == 1 && MODE == MODE_UPDATE && io.ctid == IOT && j >= 1 && ne == EB) {
       // tile j-1's residual store has left sRes by now (issued at the end of its epilogue)
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       load_res(j);
@@ -957,35 +999,37 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       nbar_sync(W::BAR_C, W::CT);
       if (io.ctid < 32) trace_ev(A, j, 7);
       if (io.ctid == IOT) {
-        // Q first: once its bulk read is done the input buffer is free; the residual store is
-        // waited for only before the next residual load (after the next volume contraction)
+        // Q first (its buffer is released first); neither store is waited for here: the input
+        // refill / release and (NRES == 1) the next residual load follow at the next tile's
+        // XV_FULL
         fence_proxy_async();
         tma_store_1d(A.Qout + size_t(e0) * 5 * NP, q_s, W::BQ);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         tma_store_1d(A.res + size_t(e0) * 5 * NP, sRes, W::BQ);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-        // two residual buffers: the next tile's goes where tile j-1's was stored from (that
-        // store is older than the Q store just waited for)
-        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) load_res(j + 1);
+        if (!IODEFER) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) {
+          // the next tile's residual goes where tile j-1's was stored from: every group but the
+          // two just committed has been read (issued a tile ago)
+          if (IODEFER) asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory");
+          load_res(j + 1);
+        }
       }
     }
     if (io.ctid < 32) trace_ev(A, j, 5);
-    if (W::NIN == 2) {
-      // full tiles: this thread refills the buffer (its Q store has been read, or, without a
-      // store, nobody reads it any more); the partial last tile is loaded by the producers,
-      // who wait for consumer warp 0 to signal the buffer free
-      if (io.ctid == IOT && j + 2 < io.nmine && tile_full(j + 2)) fetch_in(j + 2);
-      if (j + 2 < io.nmine && !tile_full(j + 2) && (io.ctid >> 5) == IOW) {
+    if (!IODEFER) {
+      if (W::NIN == 2) {
+        if (io.ctid == IOT && j + 2 < io.nmine && tile_full(j + 2)) fetch_in(j + 2);
+        if (j + 2 < io.nmine && !tile_full(j + 2) && (io.ctid >> 5) == IOW) {
+          __syncwarp();
+          nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
+        }
+      } else if (j + W::NIN < io.nmine && (io.ctid >> 5) == IOW) {
         __syncwarp();
         nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
       }
-    } else if (j + W::NIN < io.nmine && (io.ctid >> 5) == IOW) {
-      // only consumer warp 0 signals the Q buffer free (after BAR_C and its lane 0 saw the Q
-      // bulk read finish)
-      __syncwarp();
-      nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
     }
+    trace_w(A, j, 6);
   }
   // make the last bulk stores globally visible before the kernel ends
   if (io.ctid == IOT) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -1029,11 +1073,19 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-  // Producers take the HIGH warp ids: the SMSP arbiter issues highest-wid-first, so their
+  // Producers take the HIGH warp ids (N = 4): the SMSP arbiter issues highest-wid-first, so their
   // short FP64 chains win the shared FP64/DMMA pipe and the consumers fill the remaining slots.
-  const bool is_producer = warp >= W::CW;
+  // N = 3 (consumers the bound): the consumers take the high warp ids instead (C3 66.3 -> 67.1,
+  // C2 55.0 -> 55.3 GDOF/s; at N = 4, where the producers are the bound, 56.0 -> 54.5)
+#ifdef DG_CHI
+  constexpr bool CHI = DG_CHI;
+#else
+  constexpr bool CHI = N == 3;
+#endif
+  static_assert(!CHI || W::PW % 4 == 0, "consumer cw must run on SMSP cw % 4 (M8Plan)");
+  const bool is_producer = CHI ? warp < W::PW : warp >= W::CW;
   if (is_producer) {
-    const int ptid = tid - W::CT, pwarp = ptid >> 5;
+    const int ptid = CHI ? tid : tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
     const double gm1 = A.gamma - 1.0;
     auto fetch = [&](int jj) {
@@ -1087,7 +1139,9 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
+      trace_w(A, j, 4);
       if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
+      trace_w(A, j, 5);
       if (ptid < 32) trace_ev(A, j, 10);
       // branch-free, two nodes per thread interleaved (independent FP64 chains); slots past the
       // tile's nodes compute on a clamped node and only store zeros / nothing
@@ -1128,7 +1182,9 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       }
       // ---- face fluxes -> Xf
       if (ptid < 32) trace_ev(A, j, 12);
+      trace_w(A, j, 6);
       if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
+      trace_w(A, j, 7);
       if (ptid < 32) trace_ev(A, j, 13);
       face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
       if (ptid < 32) trace_ev(A, j, 14);
@@ -1140,8 +1196,8 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     // every warp runs a compile-time-shaped loop over its units so its DMMA chains interleave
     // without run-time branches
     using PL = M8Plan<N>;
-    const int cw = warp;
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, tid, lane};
+    const int cw = CHI ? warp - W::PW : warp;   // W::PW % 4 == 0: consumer cw still runs on SMSP cw % 4
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, CHI ? tid - W::PT : tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;

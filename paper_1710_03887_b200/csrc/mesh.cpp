@@ -416,8 +416,9 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
   // per k-step (OPW doubles, one contiguous block so the kernels can stream it in chunks):
   // NPG n-tile pairs of 64 doubles, lane l holding B(4ks+l%4, 8(2p)+l/4) and B(.., 8(2p+1)+l/4)
   // adjacent; then, for odd NTL, the trailing n-tile compacted to the lanes of its GS real
-  // columns (l < 4 GS)
+  // columns (l < 4 GS; for GS == 4 at N <= 4 transposed to [k = l % 4][column])
   const int NPG = NTL / 2, GS = (NTL % 2) ? Np - 8 * (NTL - 1) : 0, OPW = NPG * 64 + 4 * GS;
+  const bool sbt = GS == 4 && N <= 4;
   c->opfrag.assign(size_t(KS4) * OPW, 0.0);
   for (int ks = 0; ks < KS4; ++ks) {
     double* o = c->opfrag.data() + size_t(ks) * OPW;
@@ -425,10 +426,11 @@ dg_status build_ctx(const dg_mesh_desc* d, int rank, dg_ctx* c) {
       const int g = lane >> 2, t = lane & 3;
       for (int p = 0; p < NPG; ++p)
         for (int h = 0; h < 2; ++h) o[p * 64 + 2 * lane + h] = op(8 * (2 * p + h) + g, 4 * ks + t);
-      if (lane < 4 * GS) o[NPG * 64 + lane] = op(8 * (NTL - 1) + g, 4 * ks + t);
+      // (GS == 4 in the warp-specialised kernel, N <= 4: stored [t][c], so a lane's four columns
+      // are two adjacent 16-byte words)
+      if (lane < 4 * GS) o[NPG * 64 + (sbt ? 4 * t + g : lane)] = op(8 * (NTL - 1) + g, 4 * ks + t);
     }
   }
-  (void)N;
   return DG_OK;
 }
 

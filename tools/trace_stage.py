@@ -24,7 +24,7 @@ f.restype = C.c_int
 assert f(s.ctx, buf, 4096) == 0
 all_ = np.array(buf, dtype=np.int64)
 t = all_[:1024].reshape(64, 16)
-w = all_[1024:1024 + 48 * 64].reshape(48, 16, 4)
+w = all_[1024:1024 + 24 * 16 * 8].reshape(24, 16, 8)
 names = {0: "C start", 1: "C XVfull", 2: "C volGEMM", 3: "C XFfull", 4: "C faceGEMM", 5: "C epi", 6: "C eloop", 7: "C barC", 15: "P gathered",
          8: "P start", 9: "P tma", 10: "P XVempty", 11: "P vol", 12: "P fetch", 13: "P XFempty", 14: "P face"}
 if cfg.order >= 5:
@@ -39,10 +39,15 @@ for j in range(2, 8):
 per = (t[10, 0] - t[2, 0]) / 8
 print("cycles per tile (tiles 2..10):", per)
 if cfg.order <= 4:
-    print("per warp, relative to C start -- consumers: GEMMs done / singles reduced / residual ready / epilogue done; "
-          "producers: volume done / face done:")
+    print("per warp, cycles relative to the consumers' tile start (warp-0 stamp) --")
+    print("  consumers: at XV_FULL / passed / GEMMs done / singles reduced / residual ready / epilogue done / IO done")
+    print("  producers: at XV_EMPTY / passed / volume done / at XF_EMPTY / passed / face done")
     for j in range(3, 7):
         base = t[j, 0]
-        print(f"tile {j}: " + "  ".join(
-            (f"w{k}:{w[j, k, 0] - base}/{w[j, k, 2] - base}/{w[j, k, 3] - base}/{w[j, k, 1] - base}" if w[j, k, 2] else
-             f"w{k}:{w[j, k, 0] - base}/{w[j, k, 1] - base}") for k in range(16)))
+        print(f"tile {j}:")
+        for k in range(16):
+            r = w[j, k] - base
+            if (k >= 12) if cfg.order == 3 else (k < 8):   # consumer warps (high ids at N = 3)
+                print(f"  C w{k:2d}: {r[4]:6d} {r[5]:6d} {r[0]:6d} {r[2]:6d} {r[3]:6d} {r[1]:6d} {r[6]:6d}")
+            else:
+                print(f"  P w{k:2d}: {r[4]:6d} {r[5]:6d} {r[0]:6d} {r[6]:6d} {r[7]:6d} {r[1]:6d}")
