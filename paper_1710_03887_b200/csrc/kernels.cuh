@@ -116,13 +116,13 @@ __device__ __forceinline__ void trace_ev(const StageArgs& A, int j, int ev) {
   }
 }
 
-// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*24 + warp)*8 + k (k < 8), tiles < 16
+// per-warp stamps (DG_TRACE builds): slot 1024 + (tile*16 + warp)*8 + k (k < 8), tiles < 24
 __device__ __forceinline__ void trace_w(const StageArgs& A, int j, int k) {
-  if (DG_TRACE && blockIdx.x == 0 && j < 16 && A.trace) {
+  if (DG_TRACE && blockIdx.x == 0 && j < 24 && A.trace) {
     __syncwarp();
     unsigned long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 24 + (threadIdx.x >> 5)) * 8 + k] = t;
+    if ((threadIdx.x & 31) == 0) A.trace[1024 + (j * 16 + (threadIdx.x >> 5)) * 8 + k] = t;
   }
 }
 
@@ -280,16 +280,11 @@ template <int N, int NPASS>
 __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                             bool lane_ok, const double* q_s, const double* g_s, const int* n_s,
                                             const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
-                                            const uint8_t* sFm, double (&qp)[NPASS][5], int (&tag)[NPASS]) {
+                                            const uint8_t* sFm, double (&qp)[NPASS][5]) {
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
-#pragma unroll
-  for (int u = 0; u < NPASS; ++u) tag[u] = 0;
   // DG_GATHER2 (default: N <= 3; C3 61.7 -> 64.1, C2 52.0 -> 53.2 GDOF/s; at N = 4 55.6 -> 52.4)
 #ifndef DG_GATHER2
 #define DG_GATHER2 1
-#endif
-#ifndef DG_GATHER_BF
-#define DG_GATHER_BF 0
 #endif
   if constexpr (DG_GATHER2 == 2 || (DG_GATHER2 == 1 && N <= 3)) {
     // all passes' shared-memory lookups level by level (code and neighbour, then the node
@@ -312,25 +307,6 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
       node[u] = code[u] < CODE_GHOST ? int(sTbl[(f * 24 + code[u]) * NFP + ii])
                 : code[u] < CODE_BC ? int(sTblf[(f * 24 + code[u] - CODE_GHOST) * NFP + ii]) : int(sFm[f * NFP + ii]);
     }
-#if DG_GATHER_BF
-    // branch-free: every lane issues the five loads (boundary and idle lanes read a dummy, the
-    // first state row), so no lane writes a gather destination register while the warp's loads
-    // are in flight -- with a default value assigned on a side branch the idle lanes of every
-    // warp (lanes 30, 31 of the dense segments) waited for the loads to land (write-after-write
-    // on the scoreboard: 8 % of the kernel's stall samples) and the gathers' latency was not
-    // hidden behind the volume phase.  Boundary ghosts are formed in face_terms (tag != 0), from
-    // the own trace read there anyway.
-#pragma unroll
-    for (int u = 0; u < NPASS; ++u) {
-      const bool loc = code[u] < CODE_GHOST, halo = !loc && code[u] < CODE_BC;
-      const double* q2 = loc ? A.Qin + size_t(nb[u]) * 5 * NP + node[u]
-                         : halo ? A.recv + size_t(nb[u]) * 5 * NFP + node[u] : A.Qin;
-      const int str = loc ? NP : halo ? NFP : 0;
-      tag[u] = (ok[u] && code[u] >= CODE_BC) ? code[u] - CODE_BC : 0;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) qp[u][c] = __ldg(q2 + c * str);
-    }
-#else
 #pragma unroll
     for (int u = 0; u < NPASS; ++u) {
 #pragma unroll
@@ -354,7 +330,6 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
         ghost_trace(A, code[u] - CODE_BC, qm, G[0], G[1], G[2], qp[u]);
       }
     }
-#endif
   } else {
 #pragma unroll
   for (int u = 0; u < NPASS; ++u) {
@@ -389,7 +364,7 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
 template <int N, int NPASS, int SEGW, int XSF>
 __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fstride, int flim, int ne, int i,
                                            bool lane_ok, const double* q_s, const double* g_s, const uint8_t* sFm,
-                                           double (&qp)[NPASS][5], const int (&tag)[NPASS], double* sXf) {
+                                           const double (&qp)[NPASS][5], double* sXf) {
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
   if DG_SKIPQ(2) return;
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
@@ -413,11 +388,6 @@ __device__ __forceinline__ void face_terms(const StageArgs& A, int fbase, int fs
     const double nx = G[0], ny = G[1], nz = G[2];
     const double* q = q_s + e * 5 * NP + sFm[f * NFP + ii];
     const double qm0 = q[0], qm1 = q[NP], qm2 = q[2 * NP], qm3 = q[3 * NP], qm4 = q[4 * NP];
-    if constexpr (DG_GATHER_BF && (DG_GATHER2 == 2 || (DG_GATHER2 == 1 && N <= 3)))
-    if (tag[u]) {   // boundary face (branch-free gathers): the ghost from the own trace
-      const double qm[5] = {qm0, qm1, qm2, qm3, qm4};
-      ghost_trace(A, tag[u], qm, nx, ny, nz, qp[u]);
-    }
     const double rim = rcp_nr(qm0);
     const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
     const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
@@ -574,18 +544,8 @@ struct WS {
 #else
   static constexpr int CW = N == 3 ? 4 : 8;
 #endif
-  // DG_PP: the consumer warps form NG = 2 groups that take alternate tiles (ping-pong): one
-  // group's epilogue (shared-memory round trips, TMA hand-offs; no DMMA) runs while the other
-  // group contracts the next tile, so the SMSP's DMMA stream does not stop for it.  CW stays the
-  // warps of ONE group (the unit the work plan M8Plan splits a tile over).
-#ifndef DG_PP
-#define DG_PP 0
-#endif
-  static constexpr int NG = (DG_PP && N == 3) ? 2 : 1;
-  static constexpr int CWA = CW * NG;                        // all consumer warps
-  static constexpr int NT = 32 * (PW + CWA);
-  static constexpr int PT = 32 * PW, CT = 32 * CW, CTA_ = 32 * CWA;
-  static constexpr int NTG = PT + CT;                        // threads on a producer <-> group barrier
+  static constexpr int NT = 32 * (PW + CW);
+  static constexpr int PT = 32 * PW, CT = 32 * CW;
   static constexpr int ROWS = 5 * EB;                       // multiple of 8 (DMMA m8 row tiles)
   static_assert(ROWS % 8 == 0, "rows must fill DMMA m8 tiles");
   // faces per producer warp-pass: one face per power-of-two lane segment (butterfly face max)
@@ -637,11 +597,8 @@ struct WS {
   static constexpr size_t SMEM = SMEM_XV + SMEM_XF + SMEM_OP + SMEM_IN + SMEM_RES + SMEM_T + 64;
   static_assert(SMEM <= 227 * 1024, "warp-specialised tile does not fit in shared memory");
   // named barriers
-  // named barriers; the producer <-> consumer ones and BAR_C exist once per consumer group (+ g)
-  static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 2 + NG, BAR_XF_FULL = 2 + 2 * NG,
-                       BAR_XF_EMPTY = 2 + 3 * NG, BAR_Q_EMPTY = 2 + 4 * NG /* .. + NIN - 1 */,
-                       BAR_C = 2 + 4 * NG + 3;
-  static_assert(BAR_C + NG <= 16, "named barriers");
+  static constexpr int BAR_P = 1, BAR_XV_FULL = 2, BAR_XV_EMPTY = 3, BAR_XF_FULL = 4, BAR_XF_EMPTY = 5,
+                       BAR_Q_EMPTY = 6 /* .. 6 + NIN - 1 */, BAR_C = 9;
 };
 
 // consumer k-loop unroll (register pressure vs load hoisting): measured best 7 at N = 4
@@ -666,7 +623,6 @@ struct ConsumerIO {
   uint64_t* barRes;
   uint64_t* barIn;
   int nmine, ctid, lane;
-  int grp;   // consumer group (DG_PP: group g takes tiles g, g + NG, ...)
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0) {
@@ -792,10 +748,8 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
 #ifdef DG_IODEFER
   constexpr bool IODEFER = DG_IODEFER;
 #else
-  constexpr bool IODEFER = N == 3 && W::NG == 1;   // C3 66.0 -> 66.3 GDOF/s; at N = 4 (producers the bound) 56.0 -> 54.6
+  constexpr bool IODEFER = N == 3;   // C3 66.0 -> 66.3 GDOF/s; at N = 4 (producers the bound) 56.0 -> 54.6
 #endif
-  static_assert(W::NG == 1 || (W::NG == W::NRES && W::NIN == 3 && !IODEFER), "ping-pong groups own one residual buffer each");
-  const int grp = W::NG > 1 ? io.grp : 0;
   auto tile_full = [&](int jj) {
     const int e0 = A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * EB;
     return A.e_end - e0 >= EB;
@@ -820,8 +774,8 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     tma_load_1d(ib + W::BQ + W::BG, A.nbr + size_t(e0) * 4, W::BN, io.barIn + b);
     tma_load_1d(ib + W::BQ + W::BG + W::BN, A.code + size_t(e0) * 4, W::BC, io.barIn + b);
   };
-  if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > grp && tile_full(grp)) load_res(grp);
-  for (int j = grp; j < io.nmine; j += W::NG) {
+  if (MODE == MODE_UPDATE && io.ctid == IOT && io.nmine > 0 && tile_full(0)) load_res(0);
+  for (int j = 0; j < io.nmine; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
     const int e0 = A.e_begin + tile * EB;
     const int ne = min(EB, A.e_end - e0);
@@ -895,7 +849,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     };
     if (io.ctid < 32) trace_ev(A, j, 0);
     trace_w(A, j, 4);
-    nbar_sync(W::BAR_XV_FULL + grp, W::NTG);
+    nbar_sync(W::BAR_XV_FULL, NT);
     trace_w(A, j, 5);
     if (io.ctid < 32) trace_ev(A, j, 1);
     if (IODEFER && j >= 1) {
@@ -928,14 +882,14 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
     }
     kloop(KBlk<XSV, 0, S::KSV>{});
     if (io.ctid < 32) trace_ev(A, j, 2);
-    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY + grp, W::NTG);
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XV_EMPTY, NT);
 
-    nbar_sync(W::BAR_XF_FULL + grp, W::NTG);
+    nbar_sync(W::BAR_XF_FULL, NT);
     if (io.ctid < 32) trace_ev(A, j, 3);
     kloop(KBlk<XSF, S::KSV, S::KS4>{});
     if (io.ctid < 32) trace_ev(A, j, 4);
     trace_w(A, j, 0);
-    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY + grp, W::NTG);
+    if (j + 1 < io.nmine) nbar_arrive(W::BAR_XF_EMPTY, NT);
 #ifndef DG_SRED2
 #define DG_SRED2 1
 #endif
@@ -1042,7 +996,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
       // every thread that wrote the staged tiles orders its generic-proxy stores before the
       // async-proxy (TMA) reads of the bulk stores issued after the barrier
       fence_proxy_async();
-      nbar_sync(W::BAR_C + grp, W::CT);
+      nbar_sync(W::BAR_C, W::CT);
       if (io.ctid < 32) trace_ev(A, j, 7);
       if (io.ctid == IOT) {
         // Q first (its buffer is released first); neither store is waited for here: the input
@@ -1054,7 +1008,7 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         tma_store_1d(A.res + size_t(e0) * 5 * NP, sRes, W::BQ);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         if (!IODEFER) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-        if (W::NG == 1 && W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) {
+        if (W::NRES == 2 && j + 1 < io.nmine && tile_full(j + 1)) {
           // the next tile's residual goes where tile j-1's was stored from: every group but the
           // two just committed has been read (issued a tile ago)
           if (IODEFER) asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory");
@@ -1074,11 +1028,6 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
         __syncwarp();
         nbar_arrive(W::BAR_Q_EMPTY + buf, W::PT + 32);
       }
-    }
-    if (W::NG > 1 && staged && io.ctid == IOT && j + W::NG < io.nmine && tile_full(j + W::NG)) {
-      // the group's residual buffer: its store of tile j has been read -> the group's next tile
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      load_res(j + W::NG);
     }
     trace_w(A, j, 6);
   }
@@ -1134,20 +1083,9 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
   constexpr bool CHI = N == 3;
 #endif
   static_assert(!CHI || W::PW % 4 == 0, "consumer cw must run on SMSP cw % 4 (M8Plan)");
-  const bool is_producer = CHI ? warp < W::PW : warp >= W::CWA;
-  // DG_SMR_P / DG_SMR_C (experiment): re-split the register file between the roles at run time
-  // (setmaxnreg; both role ranges are whole warpgroups): producers drop to DG_SMR_P registers,
-  // consumers rise to DG_SMR_C
-#if defined(DG_SMR_P) && defined(DG_SMR_C)
-  if constexpr (W::NG > 1) {
-    static_assert(W::PW % 4 == 0 && W::CWA % 4 == 0, "setmaxnreg needs whole warpgroups");
-    static_assert(W::PW * (65536 / NT / 8 * 8 - DG_SMR_P) >= W::CWA * (DG_SMR_C - 65536 / NT / 8 * 8), "register pool");
-    if (is_producer) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(DG_SMR_P));
-    else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(DG_SMR_C));
-  }
-#endif
+  const bool is_producer = CHI ? warp < W::PW : warp >= W::CW;
   if (is_producer) {
-    const int ptid = CHI ? tid : tid - W::CTA_, pwarp = ptid >> 5;
+    const int ptid = CHI ? tid : tid - W::CT, pwarp = ptid >> 5;
     // ======================= producers: load (TMA), volume flux, face flux
     const double gm1 = A.gamma - 1.0;
     auto fetch = [&](int jj) {
@@ -1198,12 +1136,11 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       const bool lane_ok = i < NFP && seg < W::NSEG;
       const int fbase = pwarp * W::NSEG + seg;
       double qp[W::FPASS][5];
-      int ftag[W::FPASS];
-      face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp, ftag);
+      face_gather<N, W::FPASS>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, n_s, c_s, sTbl, sTblf, sFm, qp);
       if (ptid < 32) trace_ev(A, j, 15);
       // ---- volume fluxes -> Xv
       trace_w(A, j, 4);
-      if (j >= 1) nbar_sync(W::BAR_XV_EMPTY + (j - 1) % W::NG, W::NTG);
+      if (j >= 1) nbar_sync(W::BAR_XV_EMPTY, NT);
       trace_w(A, j, 5);
       if (ptid < 32) trace_ev(A, j, 10);
       // branch-free, two nodes per thread interleaved (independent FP64 chains); slots past the
@@ -1231,7 +1168,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       }
       if (ptid < 32) trace_ev(A, j, 11);
       trace_w(A, j, 0);
-      nbar_arrive(W::BAR_XV_FULL + j % W::NG, W::NTG);
+      nbar_arrive(W::BAR_XV_FULL, NT);
       // ---- prefetch the next tile's inputs (its buffer was last read by the epilogue of tile j-1;
       //      the Q_EMPTY sync also covers every producer thread having left tile j-1)
       if (W::NIN == 2) {
@@ -1246,24 +1183,21 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
       // ---- face fluxes -> Xf
       if (ptid < 32) trace_ev(A, j, 12);
       trace_w(A, j, 6);
-      if (j >= 1) nbar_sync(W::BAR_XF_EMPTY + (j - 1) % W::NG, W::NTG);
+      if (j >= 1) nbar_sync(W::BAR_XF_EMPTY, NT);
       trace_w(A, j, 7);
       if (ptid < 32) trace_ev(A, j, 13);
-      face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, ftag, sXf);
+      face_terms<N, W::FPASS, W::SEGW, XSF>(A, fbase, W::PW * W::NSEG, 4 * EB, ne, i, lane_ok, q_s, g_s, sFm, qp, sXf);
       if (ptid < 32) trace_ev(A, j, 14);
       trace_w(A, j, 1);
-      nbar_arrive(W::BAR_XF_FULL + j % W::NG, W::NTG);
+      nbar_arrive(W::BAR_XF_FULL, NT);
     }
   } else {
     // ======================= consumers: DMMA contraction + LSERK epilogue
     // every warp runs a compile-time-shaped loop over its units so its DMMA chains interleave
     // without run-time branches
     using PL = M8Plan<N>;
-    const int cwa = CHI ? warp - W::PW : warp;   // W::PW % 4 == 0: consumer cw still runs on SMSP cw % 4
-    const int grp = W::NG > 1 ? cwa / W::CW : 0, cw = cwa - grp * W::CW;
-    static_assert(W::NG == 1 || W::CW % 4 == 0, "group warps must keep cw % 4 == SMSP");
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine,
-                           (CHI ? tid - W::PT : tid) - grp * W::CT, lane, grp};
+    const int cw = CHI ? warp - W::PW : warp;   // W::PW % 4 == 0: consumer cw still runs on SMSP cw % 4
+    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, CHI ? tid - W::PT : tid, lane};
     int singles[PL::CSMAX], ns = 0;
     m8_singles<N>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
