@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "spectrum.cuh"
 #include "modal.cuh"
+#include "lo.cuh"
 
 namespace {
 
@@ -120,11 +121,41 @@ cudaError_t launch_ws_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) 
   return cudaGetLastError();
 }
 
+// N = 1, 2: one thread per element, operator in the constant bank (lo.cuh).  DG_LO_MAXN (build
+// define, default 1) is the highest order that takes this kernel; the others keep the DMMA kernels.
+#ifndef DG_LO_MAXN
+#define DG_LO_MAXN 1
+#endif
+template <int N, int MODE>
+cudaError_t launch_lo_n(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  using L = dgk::LO<N>;
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::stage_lo_kernel<N, MODE>, L::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  const int ntiles = (A.e_end - A.e_begin + L::T - 1) / L::T;
+  if (ntiles <= 0) return cudaSuccess;
+  dgk::LoOp<N> O;
+  const dgb::RefElem& R = c->ref;
+  const int Np = L::NP, Nfp = L::NFP;
+  for (int n = 0; n < Np; ++n) {
+    for (int k = 0; k < Np; ++k) {
+      O.v[(0 * Np + k) * Np + n] = -R.Dr[n * Np + k];
+      O.v[(1 * Np + k) * Np + n] = -R.Ds[n * Np + k];
+      O.v[(2 * Np + k) * Np + n] = -R.Dt[n * Np + k];
+    }
+    for (int k = 0; k < 4 * Nfp; ++k) O.v[(3 * Np + k) * Np + n] = R.LIFT[n * 4 * Nfp + k];
+  }
+  for (int i = 0; i < 4 * Nfp; ++i) O.fm[i] = R.Fmask[i];
+  dgk::stage_lo_kernel<N, MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A, O);
+  return cudaGetLastError();
+}
+
 template <int MODE>
-cudaError_t launch_stage(int N, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+cudaError_t launch_stage(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  const int N = c->N;
   switch (N) {
-    case 1: return launch_ws_n<1, MODE>(A, max_ctas, st);
-    case 2: return launch_ws_n<2, MODE>(A, max_ctas, st);
+    case 1: return DG_LO_MAXN >= 1 ? launch_lo_n<1, MODE>(c, A, max_ctas, st) : launch_ws_n<1, MODE>(A, max_ctas, st);
+    case 2: return DG_LO_MAXN >= 2 ? launch_lo_n<2, MODE>(c, A, max_ctas, st) : launch_ws_n<2, MODE>(A, max_ctas, st);
     case 3: return launch_ws_n<3, MODE>(A, max_ctas, st);
     case 4: return launch_ws_n<4, MODE>(A, max_ctas, st);
     case 5: return launch_ho_n<5, MODE>(A, max_ctas, st);
@@ -307,7 +338,7 @@ dg_status compute_stage(dg_ctx* c, int s, double dt, int which, cudaStream_t st)
   if (A.e_end > A.e_begin) {
     const int cap = launch_cap(c, which);
     CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_UPDATE>(c->N, A, cap, st)
-                                             : launch_stage<dgk::MODE_UPDATE>(c->N, A, cap, st));
+                                             : launch_stage<dgk::MODE_UPDATE>(c, A, cap, st));
     ++c->launches;
   }
   return DG_OK;
@@ -612,7 +643,7 @@ dg_status dg_rhs_compute(dg_ctx* c, double t, double* out, int which, void* stre
   set_range(c, A, which);
   if (A.e_end > A.e_begin) {
     CUDA_TRY(c, c->scheme == DG_SCHEME_MODAL ? launch_modal<dgk::MODE_RHS>(c->N, A, launch_cap(c, which), st)
-                                             : launch_stage<dgk::MODE_RHS>(c->N, A, launch_cap(c, which), st));
+                                             : launch_stage<dgk::MODE_RHS>(c, A, launch_cap(c, which), st));
     ++c->launches;
   }
   return DG_OK;

@@ -325,7 +325,7 @@ def inflow_box(N, seed=1):
 
 
 @pytest.mark.parametrize("rk", ["lserk4", "heun"])
-@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("N", [1, 2, 4])
 def test_inflow_through_the_stepper(rk, N):
     """The time-dependent inflow ghost (Eqs. 5-7; reading A24) evaluated at each
     stage time t + c_s dt inside dg_rk_step (reading A20): 40 steps with the pulse duration
@@ -366,7 +366,10 @@ def test_partition_invariance_emulated(nparts, split, cap, name, scale):
     same for dg_rhs_compute; cap: every CTA walks several tiles of each range.  N = 4 (C4),
     N = 3 (C2: dense face segments, level-by-level gathers from the halo records) and N = 2 on
     a periodic mesh (C1: the slabs wrap around)."""
-    cfg = configs.make(name, scale=scale)
+    partition_case(configs.make(name, scale=scale), nparts, split, cap)
+
+
+def partition_case(cfg, nparts, split, cap):
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
     dt = parity.oracle_dt(o, Q, 0.5)
