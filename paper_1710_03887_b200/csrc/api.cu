@@ -150,11 +150,38 @@ cudaError_t launch_lo_n(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, 
   return cudaGetLastError();
 }
 
+// N = 1, four lanes per element (lo.cuh stage_lo4_kernel); DG_LO4 = 0 keeps one thread per element
+#ifndef DG_LO4
+#define DG_LO4 1
+#endif
+template <int MODE>
+cudaError_t launch_lo4(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  using L = dgk::LO4;
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::stage_lo4_kernel<MODE>, L::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  const int ntiles = (A.e_end - A.e_begin + L::T - 1) / L::T;
+  if (ntiles <= 0) return cudaSuccess;
+  dgk::LoOp<1> O;
+  const dgb::RefElem& R = c->ref;
+  for (int n = 0; n < 4; ++n) {
+    for (int k = 0; k < 4; ++k) {
+      O.v[(0 + k) * 4 + n] = -R.Dr[n * 4 + k];
+      O.v[(4 + k) * 4 + n] = -R.Ds[n * 4 + k];
+      O.v[(8 + k) * 4 + n] = -R.Dt[n * 4 + k];
+    }
+    for (int k = 0; k < 12; ++k) O.v[(12 + k) * 4 + n] = R.LIFT[n * 12 + k];
+  }
+  for (int i = 0; i < 12; ++i) O.fm[i] = R.Fmask[i];
+  dgk::stage_lo4_kernel<MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A, O);
+  return cudaGetLastError();
+}
+
 template <int MODE>
 cudaError_t launch_stage(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   const int N = c->N;
   switch (N) {
-    case 1: return DG_LO_MAXN >= 1 ? launch_lo_n<1, MODE>(c, A, max_ctas, st) : launch_ws_n<1, MODE>(A, max_ctas, st);
+    case 1: return DG_LO4 ? launch_lo4<MODE>(c, A, max_ctas, st) : DG_LO_MAXN >= 1 ? launch_lo_n<1, MODE>(c, A, max_ctas, st) : launch_ws_n<1, MODE>(A, max_ctas, st);
     case 2: return DG_LO_MAXN >= 2 ? launch_lo_n<2, MODE>(c, A, max_ctas, st) : launch_ws_n<2, MODE>(A, max_ctas, st);
     case 3: return launch_ws_n<3, MODE>(A, max_ctas, st);
     case 4: return launch_ws_n<4, MODE>(A, max_ctas, st);

@@ -302,3 +302,330 @@ __global__ void __launch_bounds__(LO<N>::NT, 1) stage_lo_kernel(const StageArgs 
 }
 
 }  // namespace dgk
+
+namespace dgk {
+
+// ---------------------------------------------------------------- N = 1, four lanes per element
+// At N = 1 an element has Np = 4 nodes and 4 faces: lane (e, n) of a warp (8 elements x 4 lanes)
+// computes the volume flux of node n and the three face nodes of face n, applies its OWN columns
+// of Op = [-Dr -Ds -Dt LIFT] to them (partial sums for all four output nodes, 120 FMAs), and the
+// four lanes of an element sum their partials with a transposing butterfly (xor 1, xor 2: 15
+// 64-bit shuffles) that leaves output node n on lane n.  Against one thread per element
+// (stage_lo_kernel) the same shared-memory tile holds the same number of elements in flight,
+// but an element's latency is about a quarter, which is what bounds a kernel whose element
+// count in flight is set by shared memory (540 B per element and buffer).
+// Tiles of T = 128 elements in THREE buffers: the IO warp stores tile j, waits for the store's
+// shared-memory reads and refills the buffer with tile j + 3 while the 16 compute warps work
+// through tiles j + 1 and j + 2; compute warps never wait for each other.
+struct LO4 {
+  static constexpr int NP = 4, NFP = 3, KT = 24;
+#ifdef DG_LO4_T
+  static constexpr int T = DG_LO4_T;
+#else
+  static constexpr int T = 120;   // 15 compute warps + the IO warp = 16 warps: 128 registers per thread
+#endif
+  static constexpr int NB = 3;                                // tile buffers
+  static constexpr int CT = 4 * T, NT = CT + 32;              // compute threads + the IO warp
+  static_assert(T % 8 == 0 && NT <= 1024, "whole warps of 8 elements; tile addresses stay 16-byte aligned");
+  static constexpr uint32_t BQ = uint32_t(T) * 5 * NP * 8;
+  static constexpr uint32_t BG = uint32_t(T) * GEO * 8;
+  static constexpr uint32_t BN = uint32_t(T) * 16;
+  static constexpr uint32_t BC = uint32_t(T) * 4;
+  static constexpr uint32_t BUF = 2 * BQ + BG + BN + BC;      // Q | res | geo | nbr | code
+  static constexpr size_t SMEM_OP = 4 * KT * 8;               // [lane n][24] operator columns
+  static constexpr size_t SMEM_T = size_t(2 * 96 * NFP + 15) / 16 * 16;
+  static constexpr size_t SMEM = NB * size_t(BUF) + SMEM_OP + SMEM_T + 32 + 80;   // + barriers + ghost states
+  static_assert(SMEM <= 227 * 1024, "tile buffers do not fit in shared memory");
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A, const LoOp<1> O) {
+  using L = LO4;
+  constexpr int NP = 4, NFP = 3, T = L::T, NT = L::NT, NB = L::NB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  auto bufQ = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF); };
+  auto bufR = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF + L::BQ); };
+  auto bufG = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF + 2 * L::BQ); };
+  auto bufN = [&](int b) { return reinterpret_cast<int*>(smem + size_t(b) * L::BUF + 2 * L::BQ + L::BG); };
+  auto bufC = [&](int b) { return reinterpret_cast<uint8_t*>(smem + size_t(b) * L::BUF + 2 * L::BQ + L::BG + L::BN); };
+  double* sOp = reinterpret_cast<double*>(smem + NB * size_t(L::BUF));
+  uint8_t* sTbl = reinterpret_cast<uint8_t*>(sOp) + L::SMEM_OP;
+  uint8_t* sTblf = sTbl + 96 * NFP;
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + L::SMEM_T);   // full[NB]
+  // ghost states that do not depend on the interior trace: [0] pass-through (Eq. 3), [1] inflow
+  // at this stage's time (Eqs. 5-7: pow and cos evaluated once per CTA, not per face node)
+  double* sGh = reinterpret_cast<double*>(sBar + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 96 * NFP; i += NT) {
+    sTbl[i] = A.tbl[i];
+    sTblf[i] = A.tblf[i];
+  }
+  // lane n's operator columns: [d][nn] = Op[nn][4 d + n] (its volume node), then [i][nn] =
+  // LIFT[nn][3 n + i] (its face)
+  if (tid < 4 * L::KT) {
+    const int n = tid / L::KT, k = tid % L::KT, nn = k & 3;
+    sOp[tid] = k < 12 ? O.v[((k >> 2) * 4 + n) * 4 + nn] : O.v[(12 + 3 * n + ((k - 12) >> 2)) * 4 + nn];
+  }
+  if (tid == 0)
+    for (int b = 0; b < NB; ++b) mbar_init(&sBar[b], 1);
+  if (tid == 32) {
+    double qi[5];
+    inflow_state(A, qi);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      sGh[c] = A.qinf[c];
+      sGh[5 + c] = qi[c];
+    }
+  }
+  __syncthreads();
+  const int ntiles = (A.e_end - A.e_begin + T - 1) / T;
+  const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * T; };
+  auto tile_full = [&](int jj) { return A.e_end - tile_e0(jj) >= T; };
+  constexpr int BAR_DONE = 1;   // named barriers 1 .. NB: buffer b's tile computed
+
+  if (warp == L::CT / 32) {
+    // ======================= IO warp
+    auto issue_load = [&](int jj) {   // lane 0; the buffer's previous bulk stores have been read
+      const int b = jj % NB;
+      if (tile_full(jj)) {
+        const size_t e0 = size_t(tile_e0(jj));
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&sBar[b], (MODE == MODE_UPDATE ? 2 * L::BQ : L::BQ) + L::BG + L::BN + L::BC);
+        tma_load_1d(bufQ(b), A.Qin + e0 * 5 * NP, L::BQ, &sBar[b]);
+        if (MODE == MODE_UPDATE) tma_load_1d(bufR(b), A.res + e0 * 5 * NP, L::BQ, &sBar[b]);
+        tma_load_1d(bufG(b), A.geo + e0 * GEO, L::BG, &sBar[b]);
+        tma_load_1d(bufN(b), A.nbr + e0 * 4, L::BN, &sBar[b]);
+        tma_load_1d(bufC(b), A.code + e0 * 4, L::BC, &sBar[b]);
+      } else {
+        // the partial last tile: its lanes fill their slots with plain loads; hand the buffer over
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&sBar[b])) : "memory");
+      }
+    };
+    if (lane == 0)
+      for (int jj = 0; jj < NB && jj < nmine; ++jj) issue_load(jj);
+    for (int j = 0; j < nmine; ++j) {
+      const int b = j % NB;
+      nbar_sync(BAR_DONE + b, NT);
+      if (lane == 0) {
+        const bool st = MODE == MODE_UPDATE && tile_full(j);
+        if (st) {
+          const size_t e0 = size_t(tile_e0(j));
+          fence_proxy_async();
+          tma_store_1d(A.Qout + e0 * 5 * NP, bufQ(b), L::BQ);
+          tma_store_1d(A.res + e0 * 5 * NP, bufR(b), L::BQ);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        if (j + NB < nmine) {
+          if (st) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          issue_load(j + NB);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    return;
+  }
+
+  // ======================= compute warps: lane (es, n) = element slot es of the tile, node / face n
+  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
+  const int es = tid >> 2, n = tid & 3;
+  const int fm0 = A.fmask[n * NFP], fm1 = A.fmask[n * NFP + 1], fm2 = A.fmask[n * NFP + 2];
+  const double* cf = sOp + n * L::KT;
+  const bool o1 = n & 1, o2 = (n & 2) != 0;
+  for (int j = 0; j < nmine; ++j) {
+    const int b = j % NB;
+    const int e0 = tile_e0(j);
+    const int ne = min(T, A.e_end - e0);
+    const bool full = ne == T;
+    double* q_s = bufQ(b) + es * 5 * NP;
+    double* r_s = bufR(b) + es * 5 * NP;
+    double* g_s = bufG(b) + es * GEO;
+    int* n_s = bufN(b) + es * 4;
+    uint8_t* c_s = bufC(b) + es * 4;
+    mbar_wait(&sBar[b], (j / NB) & 1);
+    const bool active = es < ne;
+    // slots past a partial tile's elements work on its last element and store nothing
+    const size_t eg = size_t(e0) + (active ? es : ne - 1);
+    if (!full) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) q_s[c * NP + n] = __ldg(A.Qin + eg * 5 * NP + c * NP + n);
+      for (int i = n; i < GEO; i += 4) g_s[i] = __ldg(A.geo + eg * GEO + i);
+      n_s[n] = __ldg(A.nbr + eg * 4 + n);
+      c_s[n] = A.code[eg * 4 + n];
+      __syncwarp();
+    }
+    // ---- neighbour trace of face n (issued first: the latency hides behind the volume node)
+    double qp[NFP][5];
+    const int code = c_s[n], nb = n_s[n];
+    const int tag = code >= CODE_BC ? code - CODE_BC : 0;
+    if (code < CODE_GHOST) {
+#pragma unroll
+      for (int i = 0; i < NFP; ++i) {
+        const double* q2 = A.Qin + size_t(nb) * 5 * NP + sTbl[(n * 24 + code) * NFP + i];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[i][c] = __ldg(q2 + c * NP);
+      }
+    } else if (code < CODE_BC) {
+#pragma unroll
+      for (int i = 0; i < NFP; ++i) {
+        const double* q2 = A.recv + size_t(nb) * 5 * NFP + sTblf[(n * 24 + code - CODE_GHOST) * NFP + i];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[i][c] = __ldg(q2 + c * NFP);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NFP; ++i)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[i][c] = 0.0;
+    }
+    // ---- volume node n: contravariant fluxes times this lane's columns of -Dr, -Ds, -Dt
+    double part[5][NP];
+    {
+      const double rho = q_s[n], mx = q_s[NP + n], my = q_s[2 * NP + n], mz = q_s[3 * NP + n], E = q_s[4 * NP + n];
+      const double ri = rcp_nr(rho);
+      const double u = mx * ri, v = my * ri, w = mz * ri;
+      const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
+      if (active && !state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[eg]);
+      const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double cx = g_s[3 * d], cy = g_s[3 * d + 1], cz = g_s[3 * d + 2];
+        const double U = cx * u + cy * v + cz * w;
+        double fl[5];
+        fl[0] = rho * U;
+        fl[1] = fma(cx, pd, mx * U);
+        fl[2] = fma(cy, pd, my * U);
+        fl[3] = fma(cz, pd, mz * U);
+        fl[4] = Ep * U;
+        const double2 c01 = *reinterpret_cast<const double2*>(cf + 4 * d);
+        const double2 c23 = *reinterpret_cast<const double2*>(cf + 4 * d + 2);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          part[c][0] = d == 0 ? c01.x * fl[c] : fma(c01.x, fl[c], part[c][0]);
+          part[c][1] = d == 0 ? c01.y * fl[c] : fma(c01.y, fl[c], part[c][1]);
+          part[c][2] = d == 0 ? c23.x * fl[c] : fma(c23.x, fl[c], part[c][2]);
+          part[c][3] = d == 0 ? c23.y * fl[c] : fma(c23.y, fl[c], part[c][3]);
+        }
+      }
+    }
+    // ---- face n: LLF flux with the face maximum of the wave speed, times this lane's LIFT columns
+    {
+      const double nx = g_s[9 + 4 * n], ny = g_s[9 + 4 * n + 1], nz = g_s[9 + 4 * n + 2];
+      const double hfs = 0.5 * g_s[9 + 4 * n + 3];
+      // n.F(q-) - n.F(q+) goes into the partial sums at once; only q+ - q- waits for the face max
+      double lam[NFP], dq[NFP][5];
+      double lmax = 0.0;
+#pragma unroll
+      for (int i = 0; i < NFP; ++i) {
+        const int fm = i == 0 ? fm0 : i == 1 ? fm1 : fm2;
+        const double qm0 = q_s[fm], qm1 = q_s[NP + fm], qm2 = q_s[2 * NP + fm], qm3 = q_s[3 * NP + fm], qm4 = q_s[4 * NP + fm];
+        if (tag == 1) {          // slip wall: mirror the normal momentum (Eq. 4)
+          const double mn = qm1 * nx + qm2 * ny + qm3 * nz;
+          qp[i][0] = qm0;
+          qp[i][1] = qm1 - 2.0 * mn * nx;
+          qp[i][2] = qm2 - 2.0 * mn * ny;
+          qp[i][3] = qm3 - 2.0 * mn * nz;
+          qp[i][4] = qm4;
+        } else if (tag) {        // pass-through (2) / inflow (3)
+          const double* gh = sGh + (tag == 2 ? 0 : 5);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) qp[i][c] = gh[c];
+        }
+        const double* qq = qp[i];
+        const double rim = rcp_nr(qm0);
+        const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
+        const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
+        const double rip = rcp_nr(qq[0]);
+        const double unp = (qq[1] * nx + qq[2] * ny + qq[3] * nz) * rip;
+        const double pp = gm1 * (qq[4] - 0.5 * (qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]) * rip);
+        lam[i] = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp) + sqrt_nr(gamma * pp * rip));
+        lmax = fmax(lmax, lam[i]);
+        const double dp = pm - pp;
+        double gf[5];
+        gf[0] = fma(qm0, unm, -qq[0] * unp);
+        gf[1] = fma(dp, nx, fma(qm1, unm, -qq[1] * unp));
+        gf[2] = fma(dp, ny, fma(qm2, unm, -qq[2] * unp));
+        gf[3] = fma(dp, nz, fma(qm3, unm, -qq[3] * unp));
+        gf[4] = fma(qm4 + pm, unm, -(qq[4] + pp) * unp);
+        dq[i][0] = qq[0] - qm0;
+        dq[i][1] = qq[1] - qm1;
+        dq[i][2] = qq[2] - qm2;
+        dq[i][3] = qq[3] - qm3;
+        dq[i][4] = qq[4] - qm4;
+        const double2 c01 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i);
+        const double2 c23 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i + 2);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const double g = hfs * gf[c];
+          part[c][0] = fma(c01.x, g, part[c][0]);
+          part[c][1] = fma(c01.y, g, part[c][1]);
+          part[c][2] = fma(c23.x, g, part[c][2]);
+          part[c][3] = fma(c23.y, g, part[c][3]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NFP; ++i) {
+        const double lm = hfs * (A.lambda_mode == 0 ? lmax : lam[i]);
+        const double2 c01 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i);
+        const double2 c23 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i + 2);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const double d = lm * dq[i][c];
+          part[c][0] = fma(c01.x, d, part[c][0]);
+          part[c][1] = fma(c01.y, d, part[c][1]);
+          part[c][2] = fma(c23.x, d, part[c][2]);
+          part[c][3] = fma(c23.y, d, part[c][3]);
+        }
+      }
+    }
+    // ---- sum the four lanes' partials; lane n keeps output node n (transposing butterfly)
+    double rhs[5];
+    {
+      double k0[5], k1[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const double s0 = __shfl_xor_sync(0xffffffffu, o1 ? part[c][0] : part[c][1], 1);
+        const double s1 = __shfl_xor_sync(0xffffffffu, o1 ? part[c][2] : part[c][3], 1);
+        k0[c] = (o1 ? part[c][1] : part[c][0]) + s0;   // node o1
+        k1[c] = (o1 ? part[c][3] : part[c][2]) + s1;   // node 2 + o1
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const double s = __shfl_xor_sync(0xffffffffu, o2 ? k0[c] : k1[c], 2);
+        rhs[c] = (o2 ? k1[c] : k0[c]) + s;             // node 2 o2 + o1 = n
+      }
+    }
+    // ---- LSERK update in place in the tile (full tiles), or straight to global memory
+    if (MODE == MODE_UPDATE) {
+      if (full) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const double rr = fma(A.a, r_s[c * NP + n], A.dt * rhs[c]);
+          const double qo = q_s[c * NP + n];
+          r_s[c * NP + n] = rr;
+          // every lane of the element has read the element's Q for its face by now only if the
+          // four lanes are past their face phase: they are (the butterfly's shuffles are warp-wide)
+          q_s[c * NP + n] = fma(A.b, rr, qo);
+        }
+      } else if (active) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const size_t gi = eg * 5 * NP + c * NP + n;
+          const double rr = fma(A.a, __ldg(A.res + gi), A.dt * rhs[c]);
+          A.res[gi] = rr;
+          A.Qout[gi] = fma(A.b, rr, q_s[c * NP + n]);
+        }
+      }
+    } else if (active) {
+      const size_t pe = size_t(A.pub[eg]);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) A.out[(size_t(c) * A.Kpub + pe) * NP + n] = rhs[c];
+    }
+    // order this thread's generic-proxy tile writes before the IO warp's bulk stores
+    if (MODE == MODE_UPDATE && full) fence_proxy_async();
+    nbar_arrive(BAR_DONE + b, NT);
+  }
+}
+
+}  // namespace dgk
