@@ -318,7 +318,7 @@ namespace dgk {
 // shared-memory reads and refills the buffer with tile j + 3 while the 16 compute warps work
 // through tiles j + 1 and j + 2; compute warps never wait for each other.
 struct LO4 {
-  static constexpr int NP = 4, NFP = 3, KT = 24;
+  static constexpr int NP = 4, NFP = 3, KT = 28;   // per-lane operator columns: 12 volume + 16 face
 #ifdef DG_LO4_T
   static constexpr int T = DG_LO4_T;
 #else
@@ -360,11 +360,12 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
     sTbl[i] = A.tbl[i];
     sTblf[i] = A.tblf[i];
   }
-  // lane n's operator columns: [d][nn] = Op[nn][4 d + n] (its volume node), then [i][nn] =
-  // LIFT[nn][3 n + i] (its face)
+  // lane n's operator columns: [d][nn] = Op[nn][4 d + n] (its volume node), then [f][nn] =
+  // LIFT[nn][3 f + n] (its node of face f; zero for lane 3, which has no face node)
   if (tid < 4 * L::KT) {
     const int n = tid / L::KT, k = tid % L::KT, nn = k & 3;
-    sOp[tid] = k < 12 ? O.v[((k >> 2) * 4 + n) * 4 + nn] : O.v[(12 + 3 * n + ((k - 12) >> 2)) * 4 + nn];
+    if (k < 12) sOp[tid] = O.v[((k >> 2) * 4 + n) * 4 + nn];
+    else if (k < 28) sOp[tid] = n < NFP ? O.v[(12 + 3 * ((k - 12) >> 2) + n) * 4 + nn] : 0.0;
   }
   if (tid == 0)
     for (int b = 0; b < NB; ++b) mbar_init(&sBar[b], 1);
@@ -430,7 +431,8 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
   // ======================= compute warps: lane (es, n) = element slot es of the tile, node / face n
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
   const int es = tid >> 2, n = tid & 3;
-  const int fm0 = A.fmask[n * NFP], fm1 = A.fmask[n * NFP + 1], fm2 = A.fmask[n * NFP + 2];
+  const int ii = n < NFP ? n : 0;   // face node of this lane (lane 3: node 0 again, zero LIFT columns)
+  const int fm0 = A.fmask[ii], fm1 = A.fmask[NFP + ii], fm2 = A.fmask[2 * NFP + ii], fm3 = A.fmask[3 * NFP + ii];
   const double* cf = sOp + n * L::KT;
   const bool o1 = n & 1, o2 = (n & 2) != 0;
   for (int j = 0; j < nmine; ++j) {
@@ -455,29 +457,28 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
       c_s[n] = A.code[eg * 4 + n];
       __syncwarp();
     }
-    // ---- neighbour trace of face n (issued first: the latency hides behind the volume node)
-    double qp[NFP][5];
-    const int code = c_s[n], nb = n_s[n];
-    const int tag = code >= CODE_BC ? code - CODE_BC : 0;
-    if (code < CODE_GHOST) {
+    // ---- neighbour traces (issued first: the latency hides behind the volume node).  Lane i of
+    //      the element gathers node i of ALL four faces, so the three lanes of a face read one
+    //      32-byte sector of the neighbour (one row of 4 nodes) in one wavefront per field; lane 3
+    //      rides along on node 0's addresses and its face results are weighted by zero columns
+    double qp[4][5];
+    int tagf[4];
 #pragma unroll
-      for (int i = 0; i < NFP; ++i) {
-        const double* q2 = A.Qin + size_t(nb) * 5 * NP + sTbl[(n * 24 + code) * NFP + i];
+    for (int f = 0; f < 4; ++f) {
+      const int code = c_s[f], nb = n_s[f];
+      tagf[f] = code >= CODE_BC ? code - CODE_BC : 0;
+      if (code < CODE_GHOST) {
+        const double* q2 = A.Qin + size_t(nb) * 5 * NP + sTbl[(f * 24 + code) * NFP + ii];
 #pragma unroll
-        for (int c = 0; c < 5; ++c) qp[i][c] = __ldg(q2 + c * NP);
+        for (int c = 0; c < 5; ++c) qp[f][c] = __ldg(q2 + c * NP);
+      } else if (code < CODE_BC) {
+        const double* q2 = A.recv + size_t(nb) * 5 * NFP + sTblf[(f * 24 + code - CODE_GHOST) * NFP + ii];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[f][c] = __ldg(q2 + c * NFP);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[f][c] = 0.0;
       }
-    } else if (code < CODE_BC) {
-#pragma unroll
-      for (int i = 0; i < NFP; ++i) {
-        const double* q2 = A.recv + size_t(nb) * 5 * NFP + sTblf[(n * 24 + code - CODE_GHOST) * NFP + i];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[i][c] = __ldg(q2 + c * NFP);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < NFP; ++i)
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[i][c] = 0.0;
     }
     // ---- volume node n: contravariant fluxes times this lane's columns of -Dr, -Ds, -Dt
     double part[5][NP];
@@ -509,74 +510,62 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
         }
       }
     }
-    // ---- face n: LLF flux with the face maximum of the wave speed, times this lane's LIFT columns
-    {
-      const double nx = g_s[9 + 4 * n], ny = g_s[9 + 4 * n + 1], nz = g_s[9 + 4 * n + 2];
-      const double hfs = 0.5 * g_s[9 + 4 * n + 3];
-      // n.F(q-) - n.F(q+) goes into the partial sums at once; only q+ - q- waits for the face max
-      double lam[NFP], dq[NFP][5];
-      double lmax = 0.0;
+    // ---- faces: node i of each face on lane i; LLF flux with the face maximum of the wave
+    //      speed (max over the element's lanes: two shuffles), times this lane's LIFT columns
 #pragma unroll
-      for (int i = 0; i < NFP; ++i) {
-        const int fm = i == 0 ? fm0 : i == 1 ? fm1 : fm2;
-        const double qm0 = q_s[fm], qm1 = q_s[NP + fm], qm2 = q_s[2 * NP + fm], qm3 = q_s[3 * NP + fm], qm4 = q_s[4 * NP + fm];
-        if (tag == 1) {          // slip wall: mirror the normal momentum (Eq. 4)
-          const double mn = qm1 * nx + qm2 * ny + qm3 * nz;
-          qp[i][0] = qm0;
-          qp[i][1] = qm1 - 2.0 * mn * nx;
-          qp[i][2] = qm2 - 2.0 * mn * ny;
-          qp[i][3] = qm3 - 2.0 * mn * nz;
-          qp[i][4] = qm4;
-        } else if (tag) {        // pass-through (2) / inflow (3)
-          const double* gh = sGh + (tag == 2 ? 0 : 5);
+    for (int f = 0; f < 4; ++f) {
+      const double nx = g_s[9 + 4 * f], ny = g_s[9 + 4 * f + 1], nz = g_s[9 + 4 * f + 2];
+      const double hfs = 0.5 * g_s[9 + 4 * f + 3];
+      const int fm = f == 0 ? fm0 : f == 1 ? fm1 : f == 2 ? fm2 : fm3;
+      const double qm0 = q_s[fm], qm1 = q_s[NP + fm], qm2 = q_s[2 * NP + fm], qm3 = q_s[3 * NP + fm], qm4 = q_s[4 * NP + fm];
+      if (tagf[f] == 1) {          // slip wall: mirror the normal momentum (Eq. 4)
+        const double mn = qm1 * nx + qm2 * ny + qm3 * nz;
+        qp[f][0] = qm0;
+        qp[f][1] = qm1 - 2.0 * mn * nx;
+        qp[f][2] = qm2 - 2.0 * mn * ny;
+        qp[f][3] = qm3 - 2.0 * mn * nz;
+        qp[f][4] = qm4;
+      } else if (tagf[f]) {        // pass-through (2) / inflow (3)
+        const double* gh = sGh + (tagf[f] == 2 ? 0 : 5);
 #pragma unroll
-          for (int c = 0; c < 5; ++c) qp[i][c] = gh[c];
-        }
-        const double* qq = qp[i];
-        const double rim = rcp_nr(qm0);
-        const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
-        const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
-        const double rip = rcp_nr(qq[0]);
-        const double unp = (qq[1] * nx + qq[2] * ny + qq[3] * nz) * rip;
-        const double pp = gm1 * (qq[4] - 0.5 * (qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]) * rip);
-        lam[i] = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp) + sqrt_nr(gamma * pp * rip));
-        lmax = fmax(lmax, lam[i]);
-        const double dp = pm - pp;
-        double gf[5];
-        gf[0] = fma(qm0, unm, -qq[0] * unp);
-        gf[1] = fma(dp, nx, fma(qm1, unm, -qq[1] * unp));
-        gf[2] = fma(dp, ny, fma(qm2, unm, -qq[2] * unp));
-        gf[3] = fma(dp, nz, fma(qm3, unm, -qq[3] * unp));
-        gf[4] = fma(qm4 + pm, unm, -(qq[4] + pp) * unp);
-        dq[i][0] = qq[0] - qm0;
-        dq[i][1] = qq[1] - qm1;
-        dq[i][2] = qq[2] - qm2;
-        dq[i][3] = qq[3] - qm3;
-        dq[i][4] = qq[4] - qm4;
-        const double2 c01 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i);
-        const double2 c23 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i + 2);
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          const double g = hfs * gf[c];
-          part[c][0] = fma(c01.x, g, part[c][0]);
-          part[c][1] = fma(c01.y, g, part[c][1]);
-          part[c][2] = fma(c23.x, g, part[c][2]);
-          part[c][3] = fma(c23.y, g, part[c][3]);
-        }
+        for (int c = 0; c < 5; ++c) qp[f][c] = gh[c];
       }
+      const double* qq = qp[f];
+      const double rim = rcp_nr(qm0);
+      const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
+      const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
+      const double rip = rcp_nr(qq[0]);
+      const double unp = (qq[1] * nx + qq[2] * ny + qq[3] * nz) * rip;
+      const double pp = gm1 * (qq[4] - 0.5 * (qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]) * rip);
+      double lam = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp) + sqrt_nr(gamma * pp * rip));
+      const double dp = pm - pp;
+      double gf[5], dq[5];
+      gf[0] = fma(qm0, unm, -qq[0] * unp);
+      gf[1] = fma(dp, nx, fma(qm1, unm, -qq[1] * unp));
+      gf[2] = fma(dp, ny, fma(qm2, unm, -qq[2] * unp));
+      gf[3] = fma(dp, nz, fma(qm3, unm, -qq[3] * unp));
+      gf[4] = fma(qm4 + pm, unm, -(qq[4] + pp) * unp);
+      dq[0] = qq[0] - qm0;
+      dq[1] = qq[1] - qm1;
+      dq[2] = qq[2] - qm2;
+      dq[3] = qq[3] - qm3;
+      dq[4] = qq[4] - qm4;
+      if (A.lambda_mode == 0) {    // positive doubles order like their bit patterns
+        long long a = __double_as_longlong(lam);
+        long long o = __shfl_xor_sync(0xffffffffu, a, 1);
+        a = a > o ? a : o;
+        o = __shfl_xor_sync(0xffffffffu, a, 2);
+        lam = __longlong_as_double(a > o ? a : o);
+      }
+      const double2 c01 = *reinterpret_cast<const double2*>(cf + 12 + 4 * f);
+      const double2 c23 = *reinterpret_cast<const double2*>(cf + 12 + 4 * f + 2);
 #pragma unroll
-      for (int i = 0; i < NFP; ++i) {
-        const double lm = hfs * (A.lambda_mode == 0 ? lmax : lam[i]);
-        const double2 c01 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i);
-        const double2 c23 = *reinterpret_cast<const double2*>(cf + 12 + 4 * i + 2);
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          const double d = lm * dq[i][c];
-          part[c][0] = fma(c01.x, d, part[c][0]);
-          part[c][1] = fma(c01.y, d, part[c][1]);
-          part[c][2] = fma(c23.x, d, part[c][2]);
-          part[c][3] = fma(c23.y, d, part[c][3]);
-        }
+      for (int c = 0; c < 5; ++c) {
+        const double dF = hfs * fma(lam, dq[c], gf[c]);
+        part[c][0] = fma(c01.x, dF, part[c][0]);
+        part[c][1] = fma(c01.y, dF, part[c][1]);
+        part[c][2] = fma(c23.x, dF, part[c][2]);
+        part[c][3] = fma(c23.y, dF, part[c][3]);
       }
     }
     // ---- sum the four lanes' partials; lane n keeps output node n (transposing butterfly)
