@@ -236,11 +236,29 @@ cudaError_t launch_modal_tile_p(const dgk::StageArgs& A, int max_ctas, cudaStrea
   return cudaGetLastError();
 }
 
+// p = 1: four lanes per element on TMA-streamed tiles (lo.cuh modal_lo4_kernel); DG_MODAL_LO4 = 0
+// keeps the tile kernel
+#ifndef DG_MODAL_LO4
+#define DG_MODAL_LO4 1
+#endif
+template <int MODE>
+cudaError_t launch_modal_lo4(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  using L = dgk::ML4;
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::modal_lo4_kernel<MODE>, L::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  const int ntiles = (A.e_end - A.e_begin + L::T - 1) / L::T;
+  if (ntiles <= 0) return cudaSuccess;
+  dgk::modal_lo4_kernel<MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A);
+  return cudaGetLastError();
+}
+
 #ifndef DG_MODAL_TILE
 #define DG_MODAL_TILE 1
 #endif
 template <int MODE>
 cudaError_t launch_modal(int P, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
+  if (DG_MODAL_LO4 && P == 1) return launch_modal_lo4<MODE>(A, max_ctas, st);
   if (DG_MODAL_TILE) {
     switch (P) {
       case 1: return launch_modal_tile_p<1, MODE>(A, max_ctas, st);
