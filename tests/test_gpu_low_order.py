@@ -116,3 +116,36 @@ def test_low_order_graph_replay_bitwise(monkeypatch):
         outs.append(s.get_state())
         s.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+# ---- the paper's modal-quadrature scheme at p = 1 (csrc/lo.cuh modal_lo4_kernel)
+def _modal_solver(cfg, **kw):
+    m = cfg.mesh
+    return dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma,
+                     q_inf=cfg.q_inf, scheme=dg.DG_SCHEME_MODAL, **kw)
+
+
+@pytest.mark.parametrize("name,scale,cap,relabel", [("C4", 0.1, 1, False), ("C4", 0.1, 2, True), ("C3", 0.15, 3, False),
+                                                     ("C5", 0.1, 1, False)])
+def test_modal_p1_many_tiles(name, scale, cap, relabel):
+    """p = 1 modal scheme with every CTA walking 4-11 tiles of 120 elements (all three tile
+    buffers refilled behind bulk stores, ragged tail last): one RHS in both wave-speed modes and
+    40 LSERK4 steps against the modal oracle; horn meshes with walls and pass-through faces, a
+    periodic mesh, and unstructured-style vertex orders (carried-point face tables of every
+    reachable orientation code)."""
+    from oracle import modal
+    cfg = at_order(meshes.relabelled(name, scale) if relabel else configs.make(name, scale=scale), 1)
+    S = parity.scales(cfg)
+    for lambda_mode in (1, 0):
+        o = modal.ModalOracle(parity.oracle_mesh(cfg, lambda_mode))
+        Q = flow(cfg, o.m)
+        s = _modal_solver(cfg, lambda_mode=lambda_mode)
+        s.set_max_ctas(cap)
+        s.set_state(Q)
+        want = o.to_nodal(o.rhs(o.to_modal(Q), 0.0))
+        assert parity.e_rhs(s.rhs(0.0), want, S) <= parity.RHS_TOL
+    dt = 0.5 * parity.oracle_dt(o.m, Q, 0.5)
+    s.step(dt, 40)
+    c, _, _ = timestep.integrate(lambda cc, tt: o.rhs(cc, tt), o.to_modal(Q), 0.0, dt, 40)
+    assert parity.e_state(s.get_state(), o.to_nodal(c), S) <= parity.STATE_TOL
+    s.close()
