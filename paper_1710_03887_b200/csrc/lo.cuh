@@ -779,21 +779,27 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
       t_s[2 * n + 1] = A.mtid[eg * 8 + 2 * n + 1];
       __syncwarp();
     }
-    // ---- mode n of each face neighbour's coefficients (issued first)
-    double cn[4][5];
-    int tagf[4];
+    // ---- mode n of the face neighbours' coefficients: face 0 now (behind the volume points),
+    //      face f + 1 while face f is computed (one face of look-ahead keeps 10 registers busy,
+    //      all four at once spilled)
+    int tagf[4], nbf[4];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
-      const int code = k_s[f], nb = n_s[f];
+      const int code = k_s[f];
       tagf[f] = code >= CODE_BC ? code - CODE_BC : 0;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) cn[f][c] = 0.0;
-      if (code < CODE_GHOST) {
-        const double* q2 = A.Qin + size_t(nb) * 5 * NP + n;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) cn[f][c] = __ldg(q2 + c * NP);
-      }
+      nbf[f] = code < CODE_GHOST ? n_s[f] : -1;
     }
+    double cn[5];
+    auto gather = [&](int f) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) cn[c] = 0.0;
+      if (nbf[f] >= 0) {
+        const double* q2 = A.Qin + size_t(nbf[f]) * 5 * NP + n;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) cn[c] = __ldg(q2 + c * NP);
+      }
+    };
+    gather(0);
     // ---- volume points n and n + 4
     double part[5][NP];
 #pragma unroll
@@ -842,8 +848,9 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
       // the neighbour's 20 coefficients through the warp's scratch slot of this element
       __syncwarp();
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sc[c * NP + n] = cn[f][c];
+      for (int c = 0; c < 5; ++c) sc[c * NP + n] = cn[c];
       __syncwarp();
+      if (f < 3) gather(f + 1);
       const double* to = sT + M::O_PSTD + int(t_s[2 * f]) * NQF * NP + n * NP;
       const double* tn = sT + M::O_PSTD + int(t_s[2 * f + 1]) * NQF * NP + n * NP;
       const double2 o01 = *reinterpret_cast<const double2*>(to);
