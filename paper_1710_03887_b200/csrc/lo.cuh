@@ -461,24 +461,31 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
     //      the element gathers node i of ALL four faces, so the three lanes of a face read one
     //      32-byte sector of the neighbour (one row of 4 nodes) in one wavefront per field; lane 3
     //      rides along on node 0's addresses and its face results are weighted by zero columns
-    double qp[4][5];
+#ifndef DG_LO4_LA
+#define DG_LO4_LA 1
+#endif
+    double qp[DG_LO4_LA ? 1 : 4][5];
     int tagf[4];
+    const double* qsrc[4];
+    int qstr[4];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const int code = c_s[f], nb = n_s[f];
       tagf[f] = code >= CODE_BC ? code - CODE_BC : 0;
-      if (code < CODE_GHOST) {
-        const double* q2 = A.Qin + size_t(nb) * 5 * NP + sTbl[(f * 24 + code) * NFP + ii];
+      qsrc[f] = code < CODE_GHOST ? A.Qin + size_t(nb) * 5 * NP + sTbl[(f * 24 + code) * NFP + ii]
+                : code < CODE_BC ? A.recv + size_t(nb) * 5 * NFP + sTblf[(f * 24 + code - CODE_GHOST) * NFP + ii] : A.Qin;
+      qstr[f] = code < CODE_GHOST ? NP : code < CODE_BC ? NFP : 0;
+    }
+    // face 0 now (behind the volume node), face f + 1 while face f is computed; boundary faces
+    // read a dummy (the first state row) that the ghost below overwrites
+    auto gather = [&](int f, double (&dst)[5]) {
 #pragma unroll
-        for (int c = 0; c < 5; ++c) qp[f][c] = __ldg(q2 + c * NP);
-      } else if (code < CODE_BC) {
-        const double* q2 = A.recv + size_t(nb) * 5 * NFP + sTblf[(f * 24 + code - CODE_GHOST) * NFP + ii];
+      for (int c = 0; c < 5; ++c) dst[c] = __ldg(qsrc[f] + c * qstr[f]);
+    };
+    if (DG_LO4_LA) gather(0, qp[0]);
+    else {
 #pragma unroll
-        for (int c = 0; c < 5; ++c) qp[f][c] = __ldg(q2 + c * NFP);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) qp[f][c] = 0.0;
-      }
+      for (int f = 0; f < 4; ++f) gather(f, qp[f]);
     }
     // ---- volume node n: contravariant fluxes times this lane's columns of -Dr, -Ds, -Dt
     double part[5][NP];
@@ -517,20 +524,23 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
       const double nx = g_s[9 + 4 * f], ny = g_s[9 + 4 * f + 1], nz = g_s[9 + 4 * f + 2];
       const double hfs = 0.5 * g_s[9 + 4 * f + 3];
       const int fm = f == 0 ? fm0 : f == 1 ? fm1 : f == 2 ? fm2 : fm3;
+      double qq[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) qq[c] = qp[DG_LO4_LA ? 0 : f][c];
+      if (DG_LO4_LA && f < 3) gather(f + 1, qp[0]);
       const double qm0 = q_s[fm], qm1 = q_s[NP + fm], qm2 = q_s[2 * NP + fm], qm3 = q_s[3 * NP + fm], qm4 = q_s[4 * NP + fm];
       if (tagf[f] == 1) {          // slip wall: mirror the normal momentum (Eq. 4)
         const double mn = qm1 * nx + qm2 * ny + qm3 * nz;
-        qp[f][0] = qm0;
-        qp[f][1] = qm1 - 2.0 * mn * nx;
-        qp[f][2] = qm2 - 2.0 * mn * ny;
-        qp[f][3] = qm3 - 2.0 * mn * nz;
-        qp[f][4] = qm4;
+        qq[0] = qm0;
+        qq[1] = qm1 - 2.0 * mn * nx;
+        qq[2] = qm2 - 2.0 * mn * ny;
+        qq[3] = qm3 - 2.0 * mn * nz;
+        qq[4] = qm4;
       } else if (tagf[f]) {        // pass-through (2) / inflow (3)
         const double* gh = sGh + (tagf[f] == 2 ? 0 : 5);
 #pragma unroll
-        for (int c = 0; c < 5; ++c) qp[f][c] = gh[c];
+        for (int c = 0; c < 5; ++c) qq[c] = gh[c];
       }
-      const double* qq = qp[f];
       const double rim = rcp_nr(qm0);
       const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
       const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
