@@ -270,23 +270,40 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
       const double* Gf = gS + e * GEO + 9 + 4 * f;
       const double* to = ftab(tS[e * 8 + 2 * f]) + q * NP;
       const double* c_s = cS + e * 5 * NP;
+      // 16-byte loads (Np is even, rows 16-byte aligned): half the shared-memory instructions of
+      // the dot products, which bound this phase (DG_MDV2, p = 2: 13.0 -> see DESIGN.md)
+      static_assert(NP % 2 == 0, "two modes per 16-byte load");
+      double2 tov[NP / 2];
+#pragma unroll
+      for (int i = 0; i < NP / 2; ++i) tov[i] = reinterpret_cast<const double2*>(to)[i];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) acc = fma(to[i], c_s[c * NP + i], acc);
-        um[rr][c] = acc;
+        for (int i = 0; i < NP / 2; ++i) {
+          const double2 cv = reinterpret_cast<const double2*>(c_s + c * NP)[i];
+          a0 = fma(tov[i].x, cv.x, a0);
+          a1 = fma(tov[i].y, cv.y, a1);
+        }
+        um[rr][c] = a0 + a1;
       }
       if (e >= ne) um[rr][0] = 1.0, um[rr][4] = 2.5;
       if (code < CODE_GHOST && e < ne) {
         const double* tn = ftab(tS[e * 8 + 2 * f + 1]) + q * NP;
         const double* cn = sCN + (e * 4 + f) * 5 * NP;
+        double2 tnv[NP / 2];
+#pragma unroll
+        for (int i = 0; i < NP / 2; ++i) tnv[i] = reinterpret_cast<const double2*>(tn)[i];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          double acc = 0.0;
+          double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-          for (int i = 0; i < NP; ++i) acc = fma(tn[i], cn[c * NP + i], acc);
-          up[rr][c] = acc;
+          for (int i = 0; i < NP / 2; ++i) {
+            const double2 cv = reinterpret_cast<const double2*>(cn + c * NP)[i];
+            a0 = fma(tnv[i].x, cv.x, a0);
+            a1 = fma(tnv[i].y, cv.y, a1);
+          }
+          up[rr][c] = a0 + a1;
         }
       } else if (e < ne) {
         ghost_trace(A, code - CODE_BC, um[rr], Gf[0], Gf[1], Gf[2], up[rr]);
@@ -404,44 +421,61 @@ __global__ void __launch_bounds__(MT<P>::NT, 1) modal_tile_kernel(const StageArg
       }
     }
     __syncthreads();
-    // ---- P3: the update (or rhs out)
-    double rhs[W::PR];
+    // ---- P3: the update (or rhs out); a thread takes two adjacent modes of a row (16-byte loads
+    //      of the face tables, the residual and the state; one round at every order)
+    constexpr int PR2 = (W::ROWS * NP / 2 + NT - 1) / NT;
+    double2 rhs[PR2];
 #pragma unroll
-    for (int rr = 0; rr < W::PR; ++rr) {
-      const int v = tid + rr * NT;
-      rhs[rr] = 0.0;
+    for (int rr = 0; rr < PR2; ++rr) {
+      const int v = 2 * (tid + rr * NT);
+      rhs[rr] = make_double2(0.0, 0.0);
       if (v >= W::ROWS * NP) break;
       const int e = v / (5 * NP);
-      double acc = sRV[v];
+      double2 acc = *reinterpret_cast<const double2*>(sRV + v);
 #pragma unroll
-      for (int kp = 1; kp < W::KP; ++kp) acc += sRV[kp * W::ROWS * NP + v];
+      for (int kp = 1; kp < W::KP; ++kp) {
+        const double2 t2 = *reinterpret_cast<const double2*>(sRV + kp * W::ROWS * NP + v);
+        acc.x += t2.x;
+        acc.y += t2.y;
+      }
       if (DG_MFP_P(P) == 0) {
         const int row = v / NP, i = v - row * NP;
         const double* fs = sFS + row * W::FSS;
-        double acc4[4] = {acc, 0.0, 0.0, 0.0};
+        double ax[4] = {acc.x, 0.0, 0.0, 0.0}, ay[4] = {acc.y, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int f = 0; f < 4; ++f) {
           const double* Pt = ftab(tS[e * 8 + 2 * f]) + i;
 #pragma unroll
-          for (int q = 0; q < NQF; ++q)
-            acc4[(f * NQF + q) & 3] = fma(-Pt[q * NP], fs[f * NQF + q], acc4[(f * NQF + q) & 3]);
+          for (int q = 0; q < NQF; ++q) {
+            const double2 pt = *reinterpret_cast<const double2*>(Pt + q * NP);
+            const double w = fs[f * NQF + q];
+            ax[(f * NQF + q) & 3] = fma(-pt.x, w, ax[(f * NQF + q) & 3]);
+            ay[(f * NQF + q) & 3] = fma(-pt.y, w, ay[(f * NQF + q) & 3]);
+          }
         }
-        acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        acc.x = (ax[0] + ax[1]) + (ax[2] + ax[3]);
+        acc.y = (ay[0] + ay[1]) + (ay[2] + ay[3]);
       }
       rhs[rr] = acc;
       if (MODE == MODE_UPDATE && e < ne) {
         const size_t gi = size_t(e0) * 5 * NP + v;
-        const double r2 = fma(A.a, A.res[gi], A.dt * acc);
-        A.res[gi] = r2;
-        A.Qout[gi] = fma(A.b, r2, cS[v]);
+        const double2 r0 = *reinterpret_cast<const double2*>(A.res + gi);
+        const double2 c0 = *reinterpret_cast<const double2*>(cS + v);
+        double2 r2, q2;
+        r2.x = fma(A.a, r0.x, A.dt * acc.x);
+        r2.y = fma(A.a, r0.y, A.dt * acc.y);
+        q2.x = fma(A.b, r2.x, c0.x);
+        q2.y = fma(A.b, r2.y, c0.y);
+        *reinterpret_cast<double2*>(A.res + gi) = r2;
+        *reinterpret_cast<double2*>(A.Qout + gi) = q2;
       }
     }
     if (MODE == MODE_RHS) {   // V (dc/dt) into the public layout, staged in the FV region
       __syncthreads();
 #pragma unroll
-      for (int rr = 0; rr < W::PR; ++rr) {
-        const int v = tid + rr * NT;
-        if (v < W::ROWS * NP) sFV[v] = rhs[rr];
+      for (int rr = 0; rr < PR2; ++rr) {
+        const int v = 2 * (tid + rr * NT);
+        if (v < W::ROWS * NP) *reinterpret_cast<double2*>(sFV + v) = rhs[rr];
       }
       __syncthreads();
       for (int v = tid; v < ne * 5 * NP; v += NT) {
