@@ -149,3 +149,39 @@ def test_modal_p1_many_tiles(name, scale, cap, relabel):
     c, _, _ = timestep.integrate(lambda cc, tt: o.rhs(cc, tt), o.to_modal(Q), 0.0, dt, 40)
     assert parity.e_state(s.get_state(), o.to_nodal(c), S) <= parity.STATE_TOL
     s.close()
+
+
+@pytest.mark.parametrize("scheme", ["nodal", "modal"])
+def test_paper_order_full_size_properties(scheme):
+    """Properties that hold at any size, on the full-size meshes in the bench launch configuration
+    (one CTA per SM, ~83 / ~22 tiles per CTA), for both p = 1 kernels of csrc/lo.cuh:
+    (1) C4 (walls + pass-through): the ambient state is steady -- rhs = 0 up to round-off (the
+        ghosts equal the interior state, the wall mirror of zero momentum is itself);
+    (2) C5 (periodic): discrete conservation -- sum_k J_k * (element mean of rhs) = 0 for all five
+        fields (the mean of a linear polynomial over a tet is the mean of its vertex values; the
+        face fluxes cancel pairwise, S:342 / `eq:dgma`), relative to sum_k J_k * mean |rhs|."""
+    mk = _modal_solver if scheme == "modal" else solver
+    cfg = at_order(configs.make("C4"), 1)
+    s = mk(cfg)
+    K, Np = s.K, s.Np
+    Q = np.empty((5, K, Np))
+    for c in range(5):
+        Q[c] = cfg.q_inf[c]
+    s.set_state(Q)
+    f = s.rhs(0.0)
+    S = parity.scales(cfg)
+    assert (np.abs(f).reshape(5, -1).max(axis=1) / S).max() <= 1e-12
+    s.close()
+    cfg = at_order(configs.make("C5"), 1)
+    o = parity.oracle_mesh(cfg)
+    s = mk(cfg)
+    Q = configs.initial_state(cfg, s.nodes())
+    Q[1] += 0.05 * Q[0] * np.sin(2 * np.pi * s.nodes()[1])     # periodic flow
+    Q[4] += 0.5 * Q[1] ** 2 / Q[0]
+    s.set_state(Q)
+    f = s.rhs(0.0)
+    J = o.geo.J
+    tot = (J[None, :] * f.mean(axis=2)).sum(axis=1)
+    ref = (J[None, :] * np.abs(f).mean(axis=2)).sum(axis=1)
+    assert np.all(np.abs(tot) <= 1e-11 * ref.max()), (tot, ref)
+    s.close()

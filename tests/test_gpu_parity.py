@@ -178,14 +178,19 @@ def test_blowup_flag_names_the_element():
     assert e.value.status == dg.DG_EBLOWUP and "element 37" in str(e.value)
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
-def test_full_size_sampled(name):
+@pytest.mark.parametrize("name,order", [("C2", 0), ("C3", 0), ("C4", 0), ("C5", 0), ("C4", 1), ("C4", 2)])
+def test_full_size_sampled(name, order):
     """Full BASELINE.json size, bench launch configuration; oracle on sampled elements: one RHS,
     then all five LSERK4 stages through dg_stage_compute.  Each stage's input state is read back
     on the sample and its neighbours, the oracle forms f on the sample from it, carries its own
     residual res_s = a_s res_(s-1) + dt f and predicts Q_(s+1) = Q_s + b_s res_s; stages 1-4 run
-    the a_s != 0 residual path in the pipelined steady state (~20-70 tiles per CTA)."""
+    the a_s != 0 residual path in the pipelined steady state (~20-70 tiles per CTA).  order = 1,
+    2: the C4 mesh at the paper's orders (`bench.py --order N`; N = 1 is the four-lane kernel of
+    csrc/lo.cuh, ~83 tiles of 120 elements per CTA through its three tile buffers)."""
     cfg = configs.make(name)
+    if order:
+        cfg.order = order
+        name = f"{name}-N{order}"
     o = parity.oracle_mesh(cfg)
     Q = configs.initial_state(cfg, o.x)
     s = solver(cfg)
