@@ -121,36 +121,7 @@ cudaError_t launch_ws_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-// N = 1, 2: one thread per element, operator in the constant bank (lo.cuh).  DG_LO_MAXN (build
-// define, default 1) is the highest order that takes this kernel; the others keep the DMMA kernels.
-#ifndef DG_LO_MAXN
-#define DG_LO_MAXN 1
-#endif
-template <int N, int MODE>
-cudaError_t launch_lo_n(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
-  using L = dgk::LO<N>;
-  static uint64_t attr = 0;
-  cudaError_t e = ensure_smem_attr(dgk::stage_lo_kernel<N, MODE>, L::SMEM, attr);
-  if (e != cudaSuccess) return e;
-  const int ntiles = (A.e_end - A.e_begin + L::T - 1) / L::T;
-  if (ntiles <= 0) return cudaSuccess;
-  dgk::LoOp<N> O;
-  const dgb::RefElem& R = c->ref;
-  const int Np = L::NP, Nfp = L::NFP;
-  for (int n = 0; n < Np; ++n) {
-    for (int k = 0; k < Np; ++k) {
-      O.v[(0 * Np + k) * Np + n] = -R.Dr[n * Np + k];
-      O.v[(1 * Np + k) * Np + n] = -R.Ds[n * Np + k];
-      O.v[(2 * Np + k) * Np + n] = -R.Dt[n * Np + k];
-    }
-    for (int k = 0; k < 4 * Nfp; ++k) O.v[(3 * Np + k) * Np + n] = R.LIFT[n * 4 * Nfp + k];
-  }
-  for (int i = 0; i < 4 * Nfp; ++i) O.fm[i] = R.Fmask[i];
-  dgk::stage_lo_kernel<N, MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A, O);
-  return cudaGetLastError();
-}
-
-// N = 1, four lanes per element (lo.cuh stage_lo4_kernel); DG_LO4 = 0 keeps one thread per element
+// N = 1, four lanes per element (lo.cuh stage_lo4_kernel); DG_LO4 = 0 keeps the DMMA kernel
 #ifndef DG_LO4
 #define DG_LO4 1
 #endif
@@ -181,8 +152,8 @@ template <int MODE>
 cudaError_t launch_stage(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   const int N = c->N;
   switch (N) {
-    case 1: return DG_LO4 ? launch_lo4<MODE>(c, A, max_ctas, st) : DG_LO_MAXN >= 1 ? launch_lo_n<1, MODE>(c, A, max_ctas, st) : launch_ws_n<1, MODE>(A, max_ctas, st);
-    case 2: return DG_LO_MAXN >= 2 ? launch_lo_n<2, MODE>(c, A, max_ctas, st) : launch_ws_n<2, MODE>(A, max_ctas, st);
+    case 1: return DG_LO4 ? launch_lo4<MODE>(c, A, max_ctas, st) : launch_ws_n<1, MODE>(A, max_ctas, st);
+    case 2: return launch_ws_n<2, MODE>(A, max_ctas, st);
     case 3: return launch_ws_n<3, MODE>(A, max_ctas, st);
     case 4: return launch_ws_n<4, MODE>(A, max_ctas, st);
     case 5: return launch_ho_n<5, MODE>(A, max_ctas, st);

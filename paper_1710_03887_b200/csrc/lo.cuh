@@ -1,25 +1,15 @@
-// sm_100a stage kernel of the nodal-DG Euler solver at the paper's own orders, N = 1 and N = 2
-// (the paper runs p = 1) -- the same fused RK stage as stage_ws_kernel
-// (kernels.cuh: volume flux Eq. 1-2; traces and ghosts Eqs. 3-7; LLF flux,
-// P:41; LSERK update), but laid out for what bounds these orders: at N = 1 a stage is 2,940 flop
-// against 864 compulsory bytes per element (3.4 flop/B, ridge 5.7), i.e. HBM-bound, and the
-// operators are 4 x 4 / 10 x 10 -- too small for the DMMA tiling of the N >= 3 kernels, whose
-// per-tile barriers and fragment traffic dominated here (36 GDOF/s, 0.24 of the HBM roofline).
-//
-// One THREAD per element, everything of the element in registers:
-//   * a dedicated IO warp streams contiguous tiles of T elements (state, residual, geometry,
-//     connectivity) into a double-buffered shared-memory tile with 1-D TMA bulk copies and
-//     writes the updated state and residual back with TMA bulk stores from the same buffer
-//     (full/done hand-offs by mbarrier and one named barrier per buffer; compute warps never
-//     wait for each other);
-//   * the operator Op = [-Dr -Ds -Dt LIFT] and the face mask are kernel parameters: they sit
-//     in the constant bank and enter the DFMAs as immediate constant operands with
-//     compile-time indices -- no shared-memory or register traffic for the operator at all;
-//   * neighbour traces are gathered with plain 8-byte loads issued before the volume phase
-//     (measured 38 clk per element and SM fully exposed, tools/gather_bench.cu: cheaper than
-//     per-neighbour TMA bulk copies, 49, or 16-byte cp.async, 87);
-//   * the face maximum of the wave speed is a thread-local max (no shuffles), the LSERK update
-//     is done in place in the tile.
+// sm_100a stage kernels for the paper's own order (the paper runs p = 1): the
+// nodal scheme at N = 1 (stage_lo4_kernel) and the paper's modal-quadrature scheme at p = 1
+// (modal_lo4_kernel) -- the same fused RK stage as stage_ws_kernel / modal_tile_kernel (volume
+// flux Eq. 1-2; traces and ghosts Eqs. 3-7; LLF flux; LSERK update),
+// laid out for what bounds this order: at N = 1 a stage is 2,940 flop against 864 compulsory
+// bytes per element (3.4 flop/B, ridge 5.7), i.e. HBM-bound, and the operators are 4 x 4 -- too
+// small for the DMMA tiling of the N >= 2 kernels, whose per-tile barriers and fragment traffic
+// dominated here (36 GDOF/s, 0.24 of the HBM roofline).  Four lanes per element, tiles streamed
+// by TMA through three shared-memory buffers with a dedicated IO warp, no barrier between compute
+// warps.  (A one-thread-per-element version with the operator as constant-bank immediates
+// measured 54 GDOF/s at N = 1 -- latency-bound: shared memory fixes the elements in flight -- and
+// 21 at N = 2 (spills); it is in the git history of round 2.)
 // Per-element arithmetic does not depend on tile, CTA or partition (bitwise partition
 // invariance holds as for the other kernels).
 #pragma once
@@ -27,296 +17,30 @@
 
 namespace dgk {
 
-template <int N>
-struct LO {
-  using S = Shape<N>;
-  static constexpr int NP = S::NP, NFP = S::NFP;
-  static constexpr int KV = 3 * NP, KT = KV + 4 * NFP;       // unpadded operator columns
-#ifdef DG_LO_T
-  static constexpr int T = DG_LO_T;
-#else
-  static constexpr int T = N == 1 ? 192 : 96;                // elements per tile == compute threads
-#endif
-  static constexpr int NT = T + 32;                          // + the IO warp
-  static_assert(T % 32 == 0, "whole warps; keeps the TMA tile addresses 16-byte aligned");
-  static constexpr uint32_t BQ = uint32_t(T) * 5 * NP * 8;
-  static constexpr uint32_t BG = uint32_t(T) * GEO * 8;
-  static constexpr uint32_t BN = uint32_t(T) * 16;
-  static constexpr uint32_t BC = uint32_t(T) * 4;
-  static constexpr uint32_t BUF = 2 * BQ + BG + BN + BC;     // Q | res | geo | nbr | code
-  static_assert(BQ % 16 == 0 && BG % 16 == 0 && BN % 16 == 0 && BC % 16 == 0, "TMA sizes");
-  static constexpr size_t SMEM_T = size_t(2 * 96 * NFP + 15) / 16 * 16;
-  static constexpr size_t SMEM = 2 * size_t(BUF) + SMEM_T + 64;
-  static_assert(SMEM <= 227 * 1024, "low-order tile does not fit in shared memory");
-};
-
-// kernel-parameter operator: v[k * NP + n] = Op[n][k], k < 3 Np: -Dr, -Ds, -Dt; then LIFT
+// kernel-parameter operator (constant bank): v[k * 4 + n] = Op[n][k], k < 12: -Dr, -Ds, -Dt; then LIFT
 template <int N>
 struct LoOp {
-  double v[LO<N>::KT * LO<N>::NP];
-  int fm[4 * LO<N>::NFP];
+  static_assert(N == 1, "the four-lane kernel is the N = 1 kernel");
+  double v[24 * 4];
+  int fm[12];
 };
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(LO<N>::NT, 1) stage_lo_kernel(const StageArgs A, const LoOp<N> O) {
-  using L = LO<N>;
-  constexpr int NP = L::NP, NFP = L::NFP, T = L::T, NT = L::NT, KV = L::KV;
-  extern __shared__ __align__(128) unsigned char smem[];
-  auto bufQ = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF); };
-  auto bufR = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF + L::BQ); };
-  auto bufG = [&](int b) { return reinterpret_cast<double*>(smem + size_t(b) * L::BUF + 2 * L::BQ); };
-  auto bufN = [&](int b) { return reinterpret_cast<int*>(smem + size_t(b) * L::BUF + 2 * L::BQ + L::BG); };
-  auto bufC = [&](int b) { return reinterpret_cast<uint8_t*>(smem + size_t(b) * L::BUF + 2 * L::BQ + L::BG + L::BN); };
-  uint8_t* sTbl = smem + 2 * size_t(L::BUF);
-  uint8_t* sTblf = sTbl + 96 * NFP;
-  uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + L::SMEM_T);   // full[0], full[1]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < 96 * NFP; i += NT) {
-    sTbl[i] = A.tbl[i];
-    sTblf[i] = A.tblf[i];
-  }
-  if (tid == 0) {
-    mbar_init(&sBar[0], 1);
-    mbar_init(&sBar[1], 1);
-  }
-  __syncthreads();
-  const int ntiles = (A.e_end - A.e_begin + T - 1) / T;
-  const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * T; };
-  auto tile_full = [&](int jj) { return A.e_end - tile_e0(jj) >= T; };
-  constexpr int BAR_DONE = 1;   // named barriers 1, 2: buffer b's tile computed (compute arrive, IO sync)
-
-  if (warp == T / 32) {
-    // ======================= IO warp: TMA loads two tiles ahead, TMA stores behind
-    auto issue_load = [&](int jj) {   // lane 0; the buffer's previous bulk stores have been read
-      const int b = jj & 1;
-      if (tile_full(jj)) {
-        const size_t e0 = size_t(tile_e0(jj));
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&sBar[b], (MODE == MODE_UPDATE ? 2 * L::BQ : L::BQ) + L::BG + L::BN + L::BC);
-        tma_load_1d(bufQ(b), A.Qin + e0 * 5 * NP, L::BQ, &sBar[b]);
-        if (MODE == MODE_UPDATE) tma_load_1d(bufR(b), A.res + e0 * 5 * NP, L::BQ, &sBar[b]);
-        tma_load_1d(bufG(b), A.geo + e0 * GEO, L::BG, &sBar[b]);
-        tma_load_1d(bufN(b), A.nbr + e0 * 4, L::BN, &sBar[b]);
-        tma_load_1d(bufC(b), A.code + e0 * 4, L::BC, &sBar[b]);
-      } else {
-        // the partial last tile: its threads load their own slots with plain loads; only hand
-        // the (free) buffer over
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&sBar[b])) : "memory");
-      }
-    };
-    if (lane == 0) {
-      if (nmine > 0) issue_load(0);
-      if (nmine > 1) issue_load(1);
-    }
-    for (int j = 0; j < nmine; ++j) {
-      const int b = j & 1;
-      nbar_sync(BAR_DONE + b, NT);
-      if (lane == 0) {
-        const bool st = MODE == MODE_UPDATE && tile_full(j);
-        if (st) {
-          const size_t e0 = size_t(tile_e0(j));
-          fence_proxy_async();
-          tma_store_1d(A.Qout + e0 * 5 * NP, bufQ(b), L::BQ);
-          tma_store_1d(A.res + e0 * 5 * NP, bufR(b), L::BQ);
-          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        }
-        if (j + 2 < nmine) {
-          if (st) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-          issue_load(j + 2);
-        }
-      }
-      __syncwarp();
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-    return;
-  }
-
-  // ======================= compute warps: thread t owns element e0 + t of every tile
-  const double gamma = A.gamma, gm1 = A.gamma - 1.0;
-  for (int j = 0; j < nmine; ++j) {
-    const int b = j & 1;
-    const int e0 = tile_e0(j);
-    const int ne = min(T, A.e_end - e0);
-    const bool full = ne == T;
-    double* q_s = bufQ(b) + tid * 5 * NP;
-    double* r_s = bufR(b) + tid * 5 * NP;
-    double* g_s = bufG(b) + tid * GEO;
-    int* n_s = bufN(b) + tid * 4;
-    uint8_t* c_s = bufC(b) + tid * 4;
-    mbar_wait(&sBar[b], (j >> 1) & 1);
-    const bool active = tid < ne;
-    const size_t eg = size_t(e0) + tid;
-    if (!full && active) {   // partial tile: own slot by plain loads
-#pragma unroll
-      for (int i = 0; i < 5 * NP; ++i) q_s[i] = __ldg(A.Qin + eg * 5 * NP + i);
-#pragma unroll
-      for (int i = 0; i < GEO; ++i) g_s[i] = __ldg(A.geo + eg * GEO + i);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        n_s[i] = __ldg(A.nbr + eg * 4 + i);
-        c_s[i] = A.code[eg * 4 + i];
-      }
-    }
-    if (active) {
-      // ---- neighbour traces of the four faces (issued first: their latency hides behind the volume phase)
-      double qp[4][NFP][5];
-      int tag[4];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const int code = c_s[f], nb = n_s[f];
-        tag[f] = 0;
-        if (code < CODE_GHOST) {
-#pragma unroll
-          for (int i = 0; i < NFP; ++i) {
-            const double* q2 = A.Qin + size_t(nb) * 5 * NP + sTbl[(f * 24 + code) * NFP + i];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) qp[f][i][c] = __ldg(q2 + c * NP);
-          }
-        } else if (code < CODE_BC) {
-#pragma unroll
-          for (int i = 0; i < NFP; ++i) {
-            const double* q2 = A.recv + size_t(nb) * 5 * NFP + sTblf[(f * 24 + code - CODE_GHOST) * NFP + i];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) qp[f][i][c] = __ldg(q2 + c * NFP);
-          }
-        } else {
-          tag[f] = code - CODE_BC;   // boundary ghost formed from the own trace below
-#pragma unroll
-          for (int i = 0; i < NFP; ++i)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) qp[f][i][c] = 0.0;
-        }
-      }
-      // ---- volume: contravariant fluxes node by node, contracted at once with -Dr, -Ds, -Dt
-      double rhs[5][NP];
-#pragma unroll
-      for (int c = 0; c < 5; ++c)
-#pragma unroll
-        for (int n = 0; n < NP; ++n) rhs[c][n] = 0.0;
-#pragma unroll
-      for (int m = 0; m < NP; ++m) {
-        const double rho = q_s[m], mx = q_s[NP + m], my = q_s[2 * NP + m], mz = q_s[3 * NP + m], E = q_s[4 * NP + m];
-        const double ri = rcp_nr(rho);
-        const double u = mx * ri, v = my * ri, w = mz * ri;
-        const double p = gm1 * (E - 0.5 * (mx * u + my * v + mz * w));
-        if (!state_ok(rho, p, mx, my, mz, E)) flag_blowup(A.flag, A.gid[eg]);
-        const double Ep = E + p, pd = p - A.pref;   // background-flux subtraction (A14)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const double cx = g_s[3 * d], cy = g_s[3 * d + 1], cz = g_s[3 * d + 2];
-          const double U = cx * u + cy * v + cz * w;
-          double fl[5];
-          fl[0] = rho * U;
-          fl[1] = fma(cx, pd, mx * U);
-          fl[2] = fma(cy, pd, my * U);
-          fl[3] = fma(cz, pd, mz * U);
-          fl[4] = Ep * U;
-#pragma unroll
-          for (int c = 0; c < 5; ++c)
-#pragma unroll
-            for (int n = 0; n < NP; ++n) rhs[c][n] = fma(O.v[(d * NP + m) * NP + n], fl[c], rhs[c][n]);
-        }
-      }
-      // ---- faces: LLF flux with the face maximum of the wave speed, lifted at once
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const double nx = g_s[9 + 4 * f], ny = g_s[9 + 4 * f + 1], nz = g_s[9 + 4 * f + 2];
-        const double hfs = 0.5 * g_s[9 + 4 * f + 3];
-        double lam[NFP], dq[NFP][5], gf[NFP][5];
-        double lmax = 0.0;
-#pragma unroll
-        for (int i = 0; i < NFP; ++i) {
-          const int fm = O.fm[f * NFP + i];
-          const double qm0 = q_s[fm], qm1 = q_s[NP + fm], qm2 = q_s[2 * NP + fm], qm3 = q_s[3 * NP + fm], qm4 = q_s[4 * NP + fm];
-          if (tag[f]) {
-            const double qm[5] = {qm0, qm1, qm2, qm3, qm4};
-            ghost_trace(A, tag[f], qm, nx, ny, nz, qp[f][i]);
-          }
-          const double* qq = qp[f][i];
-          const double rim = rcp_nr(qm0);
-          const double unm = (qm1 * nx + qm2 * ny + qm3 * nz) * rim;
-          const double pm = gm1 * (qm4 - 0.5 * (qm1 * qm1 + qm2 * qm2 + qm3 * qm3) * rim);
-          const double rip = rcp_nr(qq[0]);
-          const double unp = (qq[1] * nx + qq[2] * ny + qq[3] * nz) * rip;
-          const double pp = gm1 * (qq[4] - 0.5 * (qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]) * rip);
-          lam[i] = fmax(fabs(unm) + sqrt_nr(gamma * pm * rim), fabs(unp) + sqrt_nr(gamma * pp * rip));
-          lmax = fmax(lmax, lam[i]);
-          const double dp = pm - pp;
-          gf[i][0] = fma(qm0, unm, -qq[0] * unp);
-          gf[i][1] = fma(dp, nx, fma(qm1, unm, -qq[1] * unp));
-          gf[i][2] = fma(dp, ny, fma(qm2, unm, -qq[2] * unp));
-          gf[i][3] = fma(dp, nz, fma(qm3, unm, -qq[3] * unp));
-          gf[i][4] = fma(qm4 + pm, unm, -(qq[4] + pp) * unp);
-          dq[i][0] = qq[0] - qm0;
-          dq[i][1] = qq[1] - qm1;
-          dq[i][2] = qq[2] - qm2;
-          dq[i][3] = qq[3] - qm3;
-          dq[i][4] = qq[4] - qm4;
-        }
-#pragma unroll
-        for (int i = 0; i < NFP; ++i) {
-          const double lm = A.lambda_mode == 0 ? lmax : lam[i];
-#pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            const double dF = hfs * fma(lm, dq[i][c], gf[i][c]);
-#pragma unroll
-            for (int n = 0; n < NP; ++n) rhs[c][n] = fma(O.v[(KV + f * NFP + i) * NP + n], dF, rhs[c][n]);
-          }
-        }
-      }
-      // ---- LSERK update in place in the tile (full tiles), or straight to global memory
-      if (MODE == MODE_UPDATE) {
-        if (full) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c)
-#pragma unroll
-            for (int n = 0; n < NP; ++n) {
-              const double rr = fma(A.a, r_s[c * NP + n], A.dt * rhs[c][n]);
-              r_s[c * NP + n] = rr;
-              q_s[c * NP + n] = fma(A.b, rr, q_s[c * NP + n]);
-            }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 5; ++c)
-#pragma unroll
-            for (int n = 0; n < NP; ++n) {
-              const size_t gi = eg * 5 * NP + c * NP + n;
-              const double rr = fma(A.a, __ldg(A.res + gi), A.dt * rhs[c][n]);
-              A.res[gi] = rr;
-              A.Qout[gi] = fma(A.b, rr, q_s[c * NP + n]);
-            }
-        }
-      } else {
-        const size_t pe = size_t(A.pub[eg]);
-#pragma unroll
-        for (int c = 0; c < 5; ++c)
-#pragma unroll
-          for (int n = 0; n < NP; ++n) A.out[(size_t(c) * A.Kpub + pe) * NP + n] = rhs[c][n];
-      }
-    }
-    // order this thread's generic-proxy tile writes before the IO warp's bulk stores
-    if (MODE == MODE_UPDATE && full) fence_proxy_async();
-    nbar_arrive(BAR_DONE + b, NT);
-  }
-}
-
-}  // namespace dgk
-
-namespace dgk {
-
 // ---------------------------------------------------------------- N = 1, four lanes per element
-// At N = 1 an element has Np = 4 nodes and 4 faces: lane (e, n) of a warp (8 elements x 4 lanes)
-// computes the volume flux of node n and the three face nodes of face n, applies its OWN columns
-// of Op = [-Dr -Ds -Dt LIFT] to them (partial sums for all four output nodes, 120 FMAs), and the
-// four lanes of an element sum their partials with a transposing butterfly (xor 1, xor 2: 15
-// 64-bit shuffles) that leaves output node n on lane n.  Against one thread per element
-// (stage_lo_kernel) the same shared-memory tile holds the same number of elements in flight,
-// but an element's latency is about a quarter, which is what bounds a kernel whose element
-// count in flight is set by shared memory (540 B per element and buffer).
-// Tiles of T = 128 elements in THREE buffers: the IO warp stores tile j, waits for the store's
-// shared-memory reads and refills the buffer with tile j + 3 while the 16 compute warps work
-// through tiles j + 1 and j + 2; compute warps never wait for each other.
+// At N = 1 an element has Np = 4 nodes and 4 faces of Nfp = 3 nodes: lane (e, n) of a warp
+// (8 elements x 4 lanes) computes the volume flux of node n and node n of EACH face (lane 3 rides
+// along on node 0's addresses; its face results meet zero LIFT columns), applies its OWN columns
+// of Op = [-Dr -Ds -Dt LIFT] to them (partial sums for all four output nodes, 120 FMAs, the
+// columns read as 16-byte shared-memory broadcasts), and the element's four lanes sum their
+// partials with a transposing butterfly (xor 1, xor 2: 15 64-bit shuffles) that leaves output
+// node n on lane n.  The kernel's elements in flight are set by shared memory (540 B per element
+// and buffer), so what counts is the latency per element: four lanes cut it to about a quarter
+// of one thread per element (54 -> 76 GDOF/s), the three lanes of a face reading ONE 32-byte
+// sector of the neighbour per field cut the gathers' L1 wavefronts from 48 to 16 per element
+// (-> 87), and gathering one face ahead freed the registers that spilled (-> 92).
+// Tiles of T = 120 elements in THREE buffers: the IO warp stores tile j, waits for the store's
+// shared-memory reads and refills the buffer with tile j + 3 while the 15 compute warps work
+// through tiles j + 1 and j + 2; compute warps never wait for each other.  16 warps in all: 128
+// registers per thread (a 17th warp would put five on one scheduler: 96 registers, spills).
 struct LO4 {
   static constexpr int NP = 4, NFP = 3, KT = 28;   // per-lane operator columns: 12 volume + 16 face
 #ifdef DG_LO4_T
