@@ -389,8 +389,12 @@ struct ML4 {
   static_assert(BQ % 16 == 0 && BG % 16 == 0 && BN % 16 == 0 && BC % 16 == 0 && BM % 16 == 0, "TMA sizes");
   static constexpr int TS = M::O_V;                              // tables kept in shared memory (doubles)
   static constexpr size_t O_T = NB * size_t(BUF);
-  static constexpr size_t O_VL = O_T + size_t(TS) * 8;           // [lane n][2 points][psi(4) | w dpsi (a, i) (12)]
-  static constexpr size_t O_SC = O_VL + 4 * 32 * 8;              // [warp][8 elements][20] neighbour coefficients
+  // per-lane volume-point columns [lane n][2 points][psi(4) | w dpsi (a, i) (12)]; lane stride 34
+  // doubles (272 B = 16 mod 128), so the four lanes' 16-byte reads fall in different banks (with
+  // 32 they were 4-way conflicts: 22 % of the kernel's shared-memory wavefronts)
+  static constexpr int VLS = 34;
+  static constexpr size_t O_VL = O_T + size_t(TS) * 8;
+  static constexpr size_t O_SC = O_VL + 4 * VLS * 8;              // [warp][8 elements][20] neighbour coefficients
   static constexpr size_t O_BAR = O_SC + size_t(CT / 32) * 8 * 20 * 8;
   static constexpr size_t SMEM = O_BAR + 32 + 80;                // full[NB] barriers, ghost states
   static_assert(SMEM <= 227 * 1024, "modal p = 1 tile buffers do not fit in shared memory");
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
   // lane n's volume-point columns: point q = n + 4 h: psi_i(q), then (w dpsi_i/dxi_a)(q) at [a][i]
   if (tid < 4 * 32) {
     const int n = tid >> 5, r = tid & 31, h = r >> 4, k = r & 15, q = n + 4 * h;
-    sVL[tid] = k < 4 ? Tg[M::O_VQ + q * NP + k] : Tg[M::O_DQ + (((k - 4) >> 2) * NP + ((k - 4) & 3)) * NQ + q];
+    sVL[n * L::VLS + r] = k < 4 ? Tg[M::O_VQ + q * NP + k] : Tg[M::O_DQ + (((k - 4) >> 2) * NP + ((k - 4) & 3)) * NQ + q];
   }
   if (tid == 0)
     for (int b = 0; b < NB; ++b) mbar_init(&sBar[b], 1);
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
   // ======================= compute warps: lane (es, n)
   const double gamma = A.gamma, gm1 = A.gamma - 1.0;
   const int es = tid >> 2, n = tid & 3;
-  const double* vl = sVL + n * 32;
+  const double* vl = sVL + n * L::VLS;
   double* sc = sSC + (warp * 8 + (lane >> 2)) * 20;
   const double wfn = sT[M::O_WF + n];
   const bool o1 = n & 1, o2 = (n & 2) != 0;
