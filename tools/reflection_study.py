@@ -15,6 +15,9 @@ horn) and C4 (horn in the truncated box, "Type B"; sensors on the +x ray from th
 bell mouth), full size, the configs' own pulses, CFL 0.5, LSERK4.
 
     python tools/reflection_study.py [C3|C4 ...] > gpurun_out/reflection_study.json
+
+A domain may be followed by the scheme and order, e.g. C3:modal:1 -- the paper's own
+modal-quadrature scheme at the paper's order p = 1 -- or C4:nodal:1.
 """
 import json
 import os
@@ -43,8 +46,12 @@ TIME_SCALE = 2.915e-5
 NEAR, REF = 0.02, 0.10     # near-boundary and reference sensors: distance from the boundary
 
 
-def run(name):
+def run(spec):
+    name, _, rest = spec.partition(":")
+    scheme, _, order = rest.partition(":")
     cfg = configs.make(name)
+    if order:
+        cfg.order = int(order)
     d = DOMAINS[name]
     m = cfg.mesh
     centre = np.array(cfg.pulses[0][2], dtype=np.float64)
@@ -52,7 +59,8 @@ def run(name):
     radii = list(d["radii"])
     pts = [centre + r * ray for r in radii]
     pts += [centre + (d["boundary"] - NEAR) * ray, centre + (d["boundary"] - REF) * ray]
-    s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma, q_inf=cfg.q_inf)
+    s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma, q_inf=cfg.q_inf,
+                  scheme=dg.DG_SCHEME_MODAL if scheme == "modal" else dg.DG_SCHEME_NODAL)
     s.set_state(configs.initial_state(cfg, s.nodes()))
     dt = s.stable_dt(cfg.cfl)
     owner = s.set_sensors(np.array(pts))
@@ -76,7 +84,7 @@ def run(name):
     band = (0.2 * f0, 2.0 * f0)
     diff, refl = analysis.reflection_indicator(db[:, 0], db[:, 1], freqs, band)
     return {
-        "domain": name, "elements": int(m.K), "order": cfg.order, "dt": dt, "steps": steps, "t_end": steps * dt,
+        "domain": name, "scheme": scheme or "nodal", "elements": int(m.K), "order": cfg.order, "dt": dt, "steps": steps, "t_end": steps * dt,
         "wall_s": round(wall, 2), "pulse": cfg.pulses[0], "sensor_points": [list(map(float, q)) for q in pts],
         "sensor_elements": [int(o) for o in owner],
         "decay": {"radii": radii, "peak_dev": [float(v) for v in dev[:nd]], "exponent": slope,
