@@ -282,11 +282,12 @@ __device__ __forceinline__ void face_gather(const StageArgs& A, int fbase, int f
                                             const uint8_t* c_s, const uint8_t* sTbl, const uint8_t* sTblf,
                                             const uint8_t* sFm, double (&qp)[NPASS][5]) {
   constexpr int NP = Shape<N>::NP, NFP = Shape<N>::NFP;
-  // DG_GATHER2 (default: N <= 3; C3 61.7 -> 64.1, C2 52.0 -> 53.2 GDOF/s; at N = 4 55.6 -> 52.4)
+  // DG_GATHER2 (default: N = 3 and N = 1; C3 61.7 -> 64.1, C2 52.0 -> 53.2 GDOF/s; at N = 4 55.6 ->
+  // 52.4; at N = 2 with 12 + 4 warps 55.2 vs 57.9 without)
 #ifndef DG_GATHER2
 #define DG_GATHER2 1
 #endif
-  if constexpr (DG_GATHER2 == 2 || (DG_GATHER2 == 1 && N <= 3)) {
+  if constexpr (DG_GATHER2 == 2 || (DG_GATHER2 == 1 && (N == 3 || N == 1))) {
     // all passes' shared-memory lookups level by level (code and neighbour, then the node
     // table), so the passes' dependent load chains overlap instead of running one after another
     int code[NPASS], nb[NPASS], node[NPASS];
@@ -527,22 +528,27 @@ __device__ __forceinline__ void vol_node(const StageArgs& A, int idx, const doub
 
 template <int N>
 struct WS {
+#ifndef DG_WS_EB2
+#define DG_WS_EB2 48
+#endif
 #ifdef DG_WS_EB
   static constexpr int EB = DG_WS_EB;
 #else
-  static constexpr int EB = (N <= 2) ? 32 : 16;
+  static constexpr int EB = N == 2 ? DG_WS_EB2 : N == 1 ? 32 : 16;
 #endif
-  // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 3 the
-  // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3)
+  // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 2, 3 the
+  // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3; N = 2 on
+  // the C4 mesh: a third of the stall samples were consumers waiting for X, 52.5 -> 54.2 GDOF/s,
+  // 57.9 with the plain face gathers)
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;
 #else
-  static constexpr int PW = N == 3 ? 12 : 8;
+  static constexpr int PW = (N == 3 || N == 2) ? 12 : 8;
 #endif
 #ifdef DG_WS_CW
   static constexpr int CW = DG_WS_CW;
 #else
-  static constexpr int CW = N == 3 ? 4 : 8;
+  static constexpr int CW = (N == 3 || N == 2) ? 4 : 8;
 #endif
   static constexpr int NT = 32 * (PW + CW);
   static constexpr int PT = 32 * PW, CT = 32 * CW;
@@ -1152,7 +1158,7 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
 #ifdef DG_SKIP_VOL
       constexpr bool SKIPV = DG_SKIP_VOL;
 #else
-      constexpr bool SKIPV = N == 3;
+      constexpr bool SKIPV = N == 3 || N == 2;   // N = 2 (EB = 48, 12 + 4 warps): 62.8 -> 65.7 GDOF/s
 #endif
 #pragma unroll
       for (int r0 = 0; r0 < VR; r0 += 2) {

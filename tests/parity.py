@@ -70,7 +70,7 @@ GRID_CAPS = (0, 2, 7)
 
 
 def tiles_per_cta(K, order, cap):
-    eb = 32 if order <= 2 else 16 if order <= 4 else 8
+    eb = 120 if order == 1 else 48 if order == 2 else 16 if order <= 4 else 8   # elements per tile
     nt = -(-K // eb)
     grid = min(nt, 148) if cap == 0 else min(nt, 148, cap)
     return -(-nt // grid)
