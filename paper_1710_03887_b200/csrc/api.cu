@@ -109,15 +109,19 @@ cudaError_t launch_ho_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-template <int N, int MODE>
+template <int N, int MODE, int V = 0>
 cudaError_t launch_ws_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
-  using W = dgk::WS<N>;
-  static uint64_t attr = 0;
-  cudaError_t e = ensure_smem_attr(dgk::stage_ws_kernel<N, MODE>, W::SMEM, attr);
-  if (e != cudaSuccess) return e;
+  using W = dgk::WS<N, V>;
   const int ntiles = (A.e_end - A.e_begin + W::EB - 1) / W::EB;
   if (ntiles <= 0) return cudaSuccess;
-  dgk::stage_ws_kernel<N, MODE><<<stage_grid(ntiles, max_ctas), W::NT, W::SMEM, st>>>(A);
+  if constexpr (N == 2 && V == 0) {
+    // small meshes: the 48-element tile would leave SMs without a tile -- the 32-element variant
+    if (ntiles < num_sms()) return launch_ws_n<N, MODE, 1>(A, max_ctas, st);
+  }
+  static uint64_t attr = 0;
+  cudaError_t e = ensure_smem_attr(dgk::stage_ws_kernel<N, MODE, V>, W::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  dgk::stage_ws_kernel<N, MODE, V><<<stage_grid(ntiles, max_ctas), W::NT, W::SMEM, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -526,7 +526,9 @@ __device__ __forceinline__ void vol_node(const StageArgs& A, int idx, const doub
   }
 }
 
-template <int N>
+// V: tile variant (N = 2 only: V = 1 is the 32-element tile for small meshes, where the 48-element
+// default leaves SMs without a tile)
+template <int N, int V = 0>
 struct WS {
 #ifndef DG_WS_EB2
 #define DG_WS_EB2 48
@@ -534,7 +536,7 @@ struct WS {
 #ifdef DG_WS_EB
   static constexpr int EB = DG_WS_EB;
 #else
-  static constexpr int EB = N == 2 ? DG_WS_EB2 : N == 1 ? 32 : 16;
+  static constexpr int EB = N == 2 ? (V == 1 ? 32 : DG_WS_EB2) : N == 1 ? 32 : 16;
 #endif
   // producer / consumer warps (DG_WS_PW / DG_WS_CW override for experiments); at N = 2, 3 the
   // flux work is the larger share, so 12 producer and 4 consumer warps (measured on C3; N = 2 on
@@ -618,7 +620,7 @@ constexpr int kunroll() {
 #endif
 }
 
-template <int N, int MODE>
+template <int N, int MODE, int V = 0>
 struct ConsumerIO {
   const StageArgs& A;
   double* sXv;
@@ -647,13 +649,13 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a0, double b0)
 #ifndef DG_SBV
 #define DG_SBV 0
 #endif
-template <int N>
+template <int N, int V = 0>
 struct M8Plan {
-  static constexpr int MT8 = WS<N>::ROWS / 8;
-  static constexpr int NPG = WS<N>::NPG, HS = WS<N>::HS;
-  static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N>::CW;
+  static constexpr int MT8 = WS<N, V>::ROWS / 8;
+  static constexpr int NPG = WS<N, V>::NPG, HS = WS<N, V>::HS;
+  static constexpr int P = MT8 * NPG, SG = MT8 * HS, CW = WS<N, V>::CW;
   static constexpr int CPMAX = (P + CW - 1) / CW;
-  static constexpr bool SDF1 = WS<N>::GS > 0 && WS<N>::GS <= 4;
+  static constexpr bool SDF1 = WS<N, V>::GS > 0 && WS<N, V>::GS <= 4;
 #ifdef DG_SWSI
   static constexpr int WSI = DG_SWSI;
 #else
@@ -706,9 +708,9 @@ struct M8Plan {
   }
 };
 
-template <int N>
+template <int N, int V = 0>
 __device__ __forceinline__ void m8_singles(int cw, int* out, int& count) {
-  using PL = M8Plan<N>;
+  using PL = M8Plan<N, V>;
   constexpr typename PL::Owners o = PL::owners();
   count = 0;
 #pragma unroll
@@ -720,11 +722,11 @@ __device__ __forceinline__ void m8_singles(int cw, int* out, int& count) {
 // epilogue in shared memory: the residual tile arrives by TMA (issued one tile ahead), res and
 // Q are updated in place and leave by two TMA bulk stores.  Partial tiles and MODE_RHS use
 // plain global accesses.
-template <int N, int MODE, int NPAIR, int NSING>
-__device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, int cw, const int* singles) {
+template <int N, int MODE, int NPAIR, int NSING, int V = 0>
+__device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE, V>& io, int cw, const int* singles) {
   using S = Shape<N>;
-  using W = WS<N>;
-  using PL = M8Plan<N>;
+  using W = WS<N, V>;
+  using PL = M8Plan<N, V>;
   constexpr int NP = S::NP, EB = W::EB, NT = W::NT, XSV = W::XSV, XSF = W::XSF;
   const StageArgs& A = io.A;
   const int lane = io.lane, g = lane >> 2, t4 = lane & 3;
@@ -1041,10 +1043,10 @@ __device__ __forceinline__ void ws_consumer_m8(const ConsumerIO<N, MODE>& io, in
   if (io.ctid == IOT) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs A) {
+template <int N, int MODE, int V = 0>
+__global__ void __launch_bounds__(WS<N, V>::NT, 1) stage_ws_kernel(const StageArgs A) {
   using S = Shape<N>;
-  using W = WS<N>;
+  using W = WS<N, V>;
   constexpr int NP = S::NP, NFP = S::NFP, EB = W::EB, NT = W::NT, PT = W::PT;
   constexpr int XSV = W::XSV, XSF = W::XSF;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1201,18 +1203,18 @@ __global__ void __launch_bounds__(WS<N>::NT, 1) stage_ws_kernel(const StageArgs 
     // ======================= consumers: DMMA contraction + LSERK epilogue
     // every warp runs a compile-time-shaped loop over its units so its DMMA chains interleave
     // without run-time branches
-    using PL = M8Plan<N>;
+    using PL = M8Plan<N, V>;
     const int cw = CHI ? warp - W::PW : warp;   // W::PW % 4 == 0: consumer cw still runs on SMSP cw % 4
-    ConsumerIO<N, MODE> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, CHI ? tid - W::PT : tid, lane};
+    ConsumerIO<N, MODE, V> io{A, sXv, sXf, sOp, in0, sRes, &sBar[W::NIN], &sBar[0], nmine, CHI ? tid - W::PT : tid, lane};
     int singles[PL::CSMAX], ns = 0;
-    m8_singles<N>(cw, singles, ns);
+    m8_singles<N, V>(cw, singles, ns);
     const int np8 = PL::P > cw ? (PL::P - 1 - cw) / PL::CW + 1 : 0;
     constexpr int CP = PL::CPMAX, CPm = PL::CPMAX > 0 ? PL::CPMAX - 1 : 0;
     // instantiate only the per-warp shapes the greedy plan can produce
     constexpr int SMAX = PL::maxcount();
 #define DG_M8_CASE(PA, SI)                                                   \
   if constexpr (PL::occurs(PA, SI)) {                                        \
-    if (np8 == PA && ns == SI) ws_consumer_m8<N, MODE, PA, SI>(io, cw, singles); \
+    if (np8 == PA && ns == SI) ws_consumer_m8<N, MODE, PA, SI, V>(io, cw, singles); \
   }
     DG_M8_CASE(CP, 0) DG_M8_CASE(CP, 1) DG_M8_CASE(CP, 2) DG_M8_CASE(CP, 3) DG_M8_CASE(CP, 4)
     DG_M8_CASE(CP, 5) DG_M8_CASE(CP, 6) DG_M8_CASE(CP, 7) DG_M8_CASE(CP, 8)

@@ -70,7 +70,9 @@ GRID_CAPS = (0, 2, 7)
 
 
 def tiles_per_cta(K, order, cap):
-    eb = 120 if order == 1 else 48 if order == 2 else 16 if order <= 4 else 8   # elements per tile
+    eb = 120 if order == 1 else 16 if order in (3, 4) else 8   # elements per tile
+    if order == 2:                       # 48, or 32 on meshes with fewer 48-element tiles than SMs
+        eb = 48 if -(-K // 48) >= 148 else 32
     nt = -(-K // eb)
     grid = min(nt, 148) if cap == 0 else min(nt, 148, cap)
     return -(-nt // grid)
