@@ -4,6 +4,9 @@ checked every `check` steps inside dg_rk_step (DG_EBLOWUP names the element), an
 summarised every `every` steps: min rho, min p, max |u|, max |p - p0| / p0.
 
     python tools/long_run.py C3 [steps] [every] > gpurun_out/long_run_C3.json
+
+The config may carry a scheme and order, e.g. C4:modal:1 (the paper's scheme at its order) or
+C4:nodal:1.
 """
 import json
 import os
@@ -22,14 +25,17 @@ from synth import configs  # noqa: E402
 
 
 def main():
-    name = sys.argv[1]
+    name, _, rest = sys.argv[1].partition(":")
+    scheme, _, order = rest.partition(":")
     cfg = configs.make(name)
+    if order:
+        cfg.order = int(order)
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.steps
     every = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, steps // 20)
     check = 10
     m = cfg.mesh
     s = dg.Solver(cfg.order, m.vxyz, m.etov, m.bc, etoe=m.etoe, etof=m.etof, gamma=cfg.gamma, q_inf=cfg.q_inf,
-                  check_every=check)
+                  check_every=check, scheme=dg.DG_SCHEME_MODAL if scheme == "modal" else dg.DG_SCHEME_NODAL)
     s.set_state(configs.initial_state(cfg, s.nodes()))
     dt = s.stable_dt(cfg.cfl)
     g = cfg.gamma
@@ -57,7 +63,7 @@ def main():
     except dg.DGError as e:
         status = str(e)
     torch.cuda.synchronize()
-    out = {"config": name, "elements": int(m.K), "order": cfg.order, "steps": n, "dt": dt, "cfl": cfg.cfl,
+    out = {"config": sys.argv[1], "elements": int(m.K), "order": cfg.order, "steps": n, "dt": dt, "cfl": cfg.cfl,
            "t_end": s.time, "check_every": check, "status": status, "wall_s": round(time.time() - t0, 2),
            "min_p_over_run": min(r["min_p"] for r in rows), "min_rho_over_run": min(r["min_rho"] for r in rows),
            "pulses": cfg.pulses, "samples": rows}
