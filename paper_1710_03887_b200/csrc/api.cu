@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "ctx.h"
 #include "kernels.cuh"
@@ -97,6 +98,23 @@ int stage_grid(int ntiles, int max_ctas) {
 }
 
 // ---------------------------------------------------------------- kernel dispatch
+// stage launch, optionally with programmatic stream serialization (kernels.cuh DG_PDL)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_stage_kernel(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int N, int MODE>
 cudaError_t launch_ho_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) {
   using H = dgk::HO<N>;
@@ -121,8 +139,8 @@ cudaError_t launch_ws_n(const dgk::StageArgs& A, int max_ctas, cudaStream_t st) 
   static uint64_t attr = 0;
   cudaError_t e = ensure_smem_attr(dgk::stage_ws_kernel<N, MODE, V>, W::SMEM, attr);
   if (e != cudaSuccess) return e;
-  dgk::stage_ws_kernel<N, MODE, V><<<stage_grid(ntiles, max_ctas), W::NT, W::SMEM, st>>>(A);
-  return cudaGetLastError();
+  return launch_stage_kernel(dgk::stage_ws_kernel<N, MODE, V>, stage_grid(ntiles, max_ctas), W::NT, W::SMEM, st,
+                             (DG_PDL >> N) & 1, A);
 }
 
 // N = 1, four lanes per element (lo.cuh stage_lo4_kernel); DG_LO4 = 0 keeps the DMMA kernel
@@ -148,8 +166,7 @@ cudaError_t launch_lo4(const dg_ctx* c, const dgk::StageArgs& A, int max_ctas, c
     for (int k = 0; k < 12; ++k) O.v[(12 + k) * 4 + n] = R.LIFT[n * 12 + k];
   }
   for (int i = 0; i < 12; ++i) O.fm[i] = R.Fmask[i];
-  dgk::stage_lo4_kernel<MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A, O);
-  return cudaGetLastError();
+  return launch_stage_kernel(dgk::stage_lo4_kernel<MODE>, stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st, (DG_PDL >> 1) & 1, A, O);
 }
 
 template <int MODE>
@@ -224,8 +241,7 @@ cudaError_t launch_modal_lo4(const dgk::StageArgs& A, int max_ctas, cudaStream_t
   if (e != cudaSuccess) return e;
   const int ntiles = (A.e_end - A.e_begin + L::T - 1) / L::T;
   if (ntiles <= 0) return cudaSuccess;
-  dgk::modal_lo4_kernel<MODE><<<stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st>>>(A);
-  return cudaGetLastError();
+  return launch_stage_kernel(dgk::modal_lo4_kernel<MODE>, stage_grid(ntiles, max_ctas), L::NT, L::SMEM, st, (DG_PDL >> 1) & 1, A);
 }
 
 #ifndef DG_MODAL_TILE

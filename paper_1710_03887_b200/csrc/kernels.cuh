@@ -162,6 +162,18 @@ __device__ __forceinline__ void inflow_state(const StageArgs& A, double (&q)[5])
 
 enum { MODE_UPDATE = 0, MODE_RHS = 1 };
 
+// Programmatic dependent launch of the stage kernels (bit N of DG_PDL: order N; default N = 1-4):
+// a stage's CTA may start on an SM as soon as the previous stage's CTA there has exited and run
+// its prologue (operator, tables, barriers, ghost states) while other SMs finish; it waits for
+// the whole previous grid (griddepcontrol.wait) before touching the state.  Hides the launch
+// latency and the prologue between the five stage launches of a step: C2 (44 us per stage) 55.1
+// -> 56.3 GDOF/s, C1 2.3 -> 2.7, C4 56.0 -> 56.2.
+#ifndef DG_PDL
+#define DG_PDL 30
+#endif
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Reciprocal and square root from the MUFU seeds plus one third-order correction each
 // (seed error e -> O(e^3), below 1 ulp for the ~2^-20 seeds): within ~1 ulp of the
 // correctly rounded results (the parity tests bound the effect), at a fraction of the
@@ -1064,6 +1076,11 @@ __global__ void __launch_bounds__(WS<N, V>::NT, 1) stage_ws_kernel(const StageAr
   uint8_t* sFm = sTblf + 96 * NFP;
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sTbl + W::SMEM_T);   // NIN inputs, then NRES residuals
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // DG_PDL (bit mask over the orders): programmatic dependent launch -- the next stage's CTA may start on this SM as
+  // soon as this CTA exits and run its prologue (operator and tables, barriers) while other SMs
+  // finish; it waits for the whole previous stage before touching the state
+  constexpr bool PDL = (DG_PDL >> N) & 1;   // DG_PDL: bit N enables it at order N
+  if (PDL) pdl_launch_dependents();
 
   // B operand (mesh.cpp layout: per k-step the n-tile pairs, then the compacted odd n-tile)
   for (int i = tid; i < W::OPC; i += NT) sOp[i] = A.op[i];
@@ -1077,6 +1094,7 @@ __global__ void __launch_bounds__(WS<N, V>::NT, 1) stage_ws_kernel(const StageAr
     for (int b = 0; b < W::NIN + W::NRES; ++b) mbar_init(&sBar[b], 1);   // inputs, then residuals
   }
   __syncthreads();
+  if (PDL) pdl_wait();
 
   const int ntiles = (A.e_end - A.e_begin + EB - 1) / EB;
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
   // at this stage's time (Eqs. 5-7: pow and cos evaluated once per CTA, not per face node)
   double* sGh = reinterpret_cast<double*>(sBar + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if ((DG_PDL >> 1) & 1) pdl_launch_dependents();
   for (int i = tid; i < 96 * NFP; i += NT) {
     sTbl[i] = A.tbl[i];
     sTblf[i] = A.tblf[i];
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(LO4::NT, 1) stage_lo4_kernel(const StageArgs A
     }
   }
   __syncthreads();
+  if ((DG_PDL >> 1) & 1) pdl_wait();
   const int ntiles = (A.e_end - A.e_begin + T - 1) / T;
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * T; };
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
   uint64_t* sBar = reinterpret_cast<uint64_t*>(smem + L::O_BAR);
   double* sGh = reinterpret_cast<double*>(sBar + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if ((DG_PDL >> 1) & 1) pdl_launch_dependents();
   const double* Tg = A.op;
   for (int i = tid; i < L::TS; i += NT) sT[i] = Tg[i];
   // lane n's volume-point columns: point q = n + 4 h: psi_i(q), then (w dpsi_i/dxi_a)(q) at [a][i]
@@ -437,6 +440,7 @@ __global__ void __launch_bounds__(ML4::NT, 1) modal_lo4_kernel(const StageArgs A
     }
   }
   __syncthreads();
+  if ((DG_PDL >> 1) & 1) pdl_wait();
   const int ntiles = (A.e_end - A.e_begin + T - 1) / T;
   const int nmine = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   auto tile_e0 = [&](int jj) { return A.e_begin + (int(blockIdx.x) + jj * int(gridDim.x)) * T; };
